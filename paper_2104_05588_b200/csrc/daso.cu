@@ -1,0 +1,613 @@
+// libdaso.so runtime: the DASO context, its NCCL communicators and the per-batch
+// step (Fig. 2-5).  Host C++; all arithmetic runs in the fused
+// kernels of kernels.cu, all communication in NCCL over NVLink / NVSwitch.
+//
+// Communicators (Fig. 1): the world comm is split into
+//   node  comm: color = node,  key = local  -> rank in node comm  == local id
+//   group comm: color = local, key = node   -> rank in group comm == node id
+// The node comm is only ever used on the caller's (compute) stream and the group
+// comm only on the library's side stream, so no communicator is driven from two
+// streams; every rank issues the same sequence of collectives on each comm because
+// every rank runs the same deterministic schedule.
+//
+// Data layout in HBM: caller-owned flat fp32 x, g, v [n_pad];
+// library-owned ring slot [P][seg] wire elements (seg = n_pad in the faithful mode,
+// n_pad / G in the sharded mode); 4-byte non-finite flag.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "daso_internal.h"
+
+struct daso_ctx {
+    int world = 0, G = 0, P = 0, rank = 0, node = 0, local = 0;
+    int device = 0;
+    daso_config cfg{};
+    daso_sched_config scfg{};
+    daso::Schedule* sched = nullptr;
+
+    ncclComm_t world_comm = nullptr, node_comm = nullptr, group_comm = nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
+
+    bool bound = false;
+    float *x = nullptr, *g = nullptr, *v = nullptr;
+    int64_t n = 0, n_pad = 0, seg = 0;
+    void* slot = nullptr;
+    size_t wire_bytes = 2;
+    uint32_t* d_flag = nullptr;
+
+    bool inflight = false;
+    int infl_group = -1, infl_S = 0;
+
+    daso_record last{};
+    std::string err;
+
+    daso_status fail(daso_status s, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return s;
+    }
+};
+
+#define CUDA_TRY(c, expr)                                                                          \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) return (c)->fail(DASO_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+#define KERN_TRY(c, expr)                                                                          \
+    do {                                                                                           \
+        int e_ = (expr);                                                                           \
+        if (e_ != 0) return (c)->fail(DASO_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(cudaError_t(e_))); \
+    } while (0)
+#define NCCL_TRY(c, expr)                                                                          \
+    do {                                                                                           \
+        ncclResult_t r_ = (expr);                                                                  \
+        if (r_ != ncclSuccess) return (c)->fail(DASO_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_)); \
+    } while (0)
+#define STATUS_TRY(expr)                  \
+    do {                                  \
+        daso_status s_ = (expr);          \
+        if (s_ != DASO_OK) return s_;     \
+    } while (0)
+
+namespace {
+
+ncclDataType_t wire_nccl(int wire) { return wire == DASO_WIRE_BF16 ? ncclBfloat16 : ncclFloat32; }
+
+// ---- state checks -----------------------------------------------------------
+daso_status poll_async(daso_ctx* c) {
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return c->fail(DASO_ERR_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
+    ncclComm_t comms[3] = {c->world_comm, c->node_comm, c->group_comm};
+    for (ncclComm_t m : comms) {
+        if (!m) continue;
+        ncclResult_t a = ncclSuccess;
+        ncclCommGetAsyncError(m, &a);
+        if (a != ncclSuccess && a != ncclInProgress)
+            return c->fail(DASO_ERR_NCCL, "asynchronous NCCL error: %s", ncclGetErrorString(a));
+    }
+    return DASO_OK;
+}
+
+daso_status require_bound(daso_ctx* c) {
+    if (!c->bound) return c->fail(DASO_ERR_PROTOCOL, "daso_bind has not been called");
+    return poll_async(c);
+}
+
+// ---- kernel argument builders --------------------------------------------------
+daso::KernelArgs base_args(daso_ctx* c, int64_t off, int64_t len, float lr) {
+    daso::KernelArgs a;
+    a.x = c->x + off;
+    a.v = c->v + off;
+    a.g = c->g + off;
+    a.n = len;
+    a.lr = lr;
+    a.mu = c->cfg.momentum;
+    a.wd = c->cfg.weight_decay;
+    a.gscale = 1.0f / float(c->G);      // Fig. 2 average = node sum x 1/G (R4)
+    a.slot = c->slot;
+    a.slot_stride = c->seg;
+    a.P = c->P;
+    a.flag = c->cfg.check_finite ? c->d_flag : nullptr;
+    return a;
+}
+
+void* own_segment(daso_ctx* c) {
+    return static_cast<char*>(c->slot) + size_t(c->node) * size_t(c->seg) * c->wire_bytes;
+}
+
+// ---- collectives ---------------------------------------------------------------
+// Non-blocking global exchange: after the packing kernel on the compute
+// stream, the side stream runs the in-place group all-gather of the slot.
+daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
+    CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
+    NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
+                              c->side));
+    CUDA_TRY(c, cudaEventRecord(c->ev_exchanged, c->side));
+    return DASO_OK;
+}
+
+daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));
+    return DASO_OK;
+}
+
+// Fig. 4 local update: the group member's parameters replace the node's.
+daso_status node_bcast(daso_ctx* c, int root, cudaStream_t s) {
+    if (c->G == 1) return DASO_OK;
+    NCCL_TRY(c, ncclBroadcast(c->x, c->x, size_t(c->n), ncclFloat32, root, c->node_comm, s));
+    return DASO_OK;
+}
+
+// ---- faithful (v1) batch ---------------------------------------------------------
+daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s) {
+    const bool global = c->P > 1;
+    if (c->G > 1)   // Fig. 2: node-local gradient sum (x 1/G in the kernel)
+        NCCL_TRY(c, ncclAllReduce(c->g, c->g, size_t(c->n), ncclFloat32, ncclSum, c->node_comm, s));
+
+    const bool merge = global && r.merge;
+    const bool merge_here = merge && c->local == r.merge_group;
+    const bool send = global && r.send;
+    const bool send_here = send && c->local == r.send_group;
+    // pack fuses into this batch's kernel unless a broadcast from another GPU
+    // replaces x in between (R11)
+    const bool fuse_pack = send_here && (!merge || r.merge_group == r.send_group);
+
+    daso::KernelArgs a = base_args(c, 0, c->n, lr);
+    int ops = daso::OP_UPDATE;
+    if (merge_here) {
+        STATUS_TRY(wait_exchange(c, s));
+        ops |= daso::OP_MERGE;
+        a.den = float(2 * r.merge_S + c->P);     // Eq. (1) denominator 2S + P
+    }
+    if (fuse_pack) {
+        ops |= daso::OP_PACK;
+        a.pack_out = own_segment(c);
+    }
+    KERN_TRY(c, daso::launch_fused(ops, c->cfg.wire, a, s));
+    if (merge) {
+        STATUS_TRY(node_bcast(c, int(r.merge_group), s));
+        c->inflight = false;
+    }
+    if (send_here && !fuse_pack) {
+        daso::KernelArgs p = base_args(c, 0, c->n, 0.f);
+        p.pack_out = own_segment(c);
+        p.flag = nullptr;
+        KERN_TRY(c, daso::launch_fused(daso::OP_PACK, c->cfg.wire, p, s));
+    }
+    if (send) {
+        if (send_here) STATUS_TRY(start_exchange(c, s));
+        if (r.blocking) {   // Fig. 3 average + Fig. 4 broadcast on the critical path
+            if (send_here) {
+                STATUS_TRY(wait_exchange(c, s));
+                daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
+                av.den = float(c->P);
+                KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+            }
+            STATUS_TRY(node_bcast(c, int(r.send_group), s));
+        } else {
+            c->inflight = true;
+            c->infl_group = int(r.send_group);
+            c->infl_S = int(r.S);
+        }
+    }
+    return DASO_OK;
+}
+
+// ---- sharded (v2) batch ----------------------------------------------------------
+// Node replicas are bitwise identical between syncs, so the update, the Eq. (1)
+// merge and the exchange are element-sharded over the node's G GPUs: reduce-scatter
+// of g, shard kernel, every group exchanges its own shard, all-gather of x.
+daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s) {
+    const bool global = c->P > 1;
+    const int64_t sh = c->seg;
+    const int64_t off = int64_t(c->local) * sh;
+    if (c->G > 1)
+        NCCL_TRY(c, ncclReduceScatter(c->g, c->g + off, size_t(sh), ncclFloat32, ncclSum, c->node_comm, s));
+    const bool merge = global && r.merge;
+    const bool send = global && r.send;
+    daso::KernelArgs a = base_args(c, off, sh, lr);
+    int ops = daso::OP_UPDATE;
+    if (merge) {
+        STATUS_TRY(wait_exchange(c, s));
+        ops |= daso::OP_MERGE;
+        a.den = float(2 * r.merge_S + c->P);
+        c->inflight = false;
+    }
+    if (send) {
+        ops |= daso::OP_PACK;
+        a.pack_out = own_segment(c);
+    }
+    KERN_TRY(c, daso::launch_fused(ops, c->cfg.wire, a, s));
+    if (send) {
+        STATUS_TRY(start_exchange(c, s));
+        if (r.blocking) {
+            STATUS_TRY(wait_exchange(c, s));
+            daso::KernelArgs av = base_args(c, off, sh, 0.f);
+            av.den = float(c->P);
+            KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+        } else {
+            c->inflight = true;
+            c->infl_group = int(r.send_group);
+            c->infl_S = int(r.S);
+        }
+    }
+    if (c->G > 1)
+        NCCL_TRY(c, ncclAllGather(c->x + off, c->x, size_t(sh), ncclFloat32, c->node_comm, s));
+    return DASO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* daso_status_string(daso_status s) {
+    switch (s) {
+        case DASO_OK: return "ok";
+        case DASO_ERR_CONFIG: return "config error";
+        case DASO_ERR_RANGE: return "range error";
+        case DASO_ERR_PROTOCOL: return "protocol error";
+        case DASO_ERR_ARGUMENT: return "argument error";
+        case DASO_ERR_CUDA: return "CUDA error";
+        case DASO_ERR_NCCL: return "NCCL error";
+        case DASO_ERR_NONFINITE: return "non-finite parameters";
+    }
+    return "unknown status";
+}
+
+const char* daso_version(void) { return "daso-b200 0.1 (sm_100a)"; }
+
+size_t daso_padded_numel(size_t n, int gpus_per_node) {
+    const size_t q = 64 * size_t(gpus_per_node < 1 ? 1 : gpus_per_node);
+    return (n + q - 1) / q * q;
+}
+
+daso_status daso_get_unique_id(void* out128) {
+    if (!out128) return DASO_ERR_ARGUMENT;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return DASO_ERR_NCCL;
+    std::memcpy(out128, &id, sizeof id);
+    return DASO_OK;
+}
+
+daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S, const daso_config* cfg,
+                      const void* uid) {
+    if (!out || !cfg || !uid) return DASO_ERR_ARGUMENT;
+    *out = nullptr;
+    if (world < 1 || gpus_per_node < 1 || world % gpus_per_node != 0 || B < 1) return DASO_ERR_CONFIG;
+    if (cfg->rank < 0 || cfg->rank >= world) return DASO_ERR_RANGE;
+    if (cfg->wire != DASO_WIRE_BF16 && cfg->wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED) return DASO_ERR_ARGUMENT;
+    daso_sched_config sc{};
+    sc.B_init = B;
+    sc.S_init = S;
+    sc.warmup_epochs = cfg->warmup_epochs;
+    sc.cooldown_epochs = cfg->cooldown_epochs;
+    sc.total_epochs = cfg->total_epochs;
+    sc.steps_per_epoch = cfg->steps_per_epoch;
+    sc.gpus_per_node = gpus_per_node;
+    if (daso::validate_sched(sc)) return DASO_ERR_CONFIG;
+
+    daso_ctx* c = new (std::nothrow) daso_ctx;
+    if (!c) return DASO_ERR_ARGUMENT;
+    c->world = world;
+    c->G = gpus_per_node;
+    c->P = world / gpus_per_node;
+    c->rank = cfg->rank;
+    c->node = cfg->rank / gpus_per_node;
+    c->local = cfg->rank % gpus_per_node;
+    c->cfg = *cfg;
+    c->scfg = sc;
+    c->sched = new daso::Schedule(sc);
+    c->wire_bytes = cfg->wire == DASO_WIRE_BF16 ? 2 : 4;
+    *out = c;   // returned even on failure so daso_last_error can be read
+
+    CUDA_TRY(c, cudaGetDevice(&c->device));
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof id);
+    ncclConfig_t wc = NCCL_CONFIG_INITIALIZER;
+    wc.blocking = 1;
+    NCCL_TRY(c, ncclCommInitRankConfig(&c->world_comm, world, id, c->rank, &wc));
+    ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+    nc.blocking = 1;
+    NCCL_TRY(c, ncclCommSplit(c->world_comm, c->node, c->local, &c->node_comm, &nc));
+    ncclConfig_t gc = NCCL_CONFIG_INITIALIZER;
+    gc.blocking = 1;
+    if (cfg->nccl_max_ctas > 0) {
+        gc.maxCTAs = cfg->nccl_max_ctas;
+        gc.minCTAs = 1;
+    }
+    NCCL_TRY(c, ncclCommSplit(c->world_comm, c->local, c->node, &c->group_comm, &gc));
+
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_exchanged, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaMalloc(&c->d_flag, sizeof(uint32_t)));
+    CUDA_TRY(c, cudaMemset(c->d_flag, 0, sizeof(uint32_t)));
+    return DASO_OK;
+}
+
+daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    if (c->bound) return c->fail(DASO_ERR_PROTOCOL, "daso_bind called twice");
+    if (!x || !g || !v || n == 0) return c->fail(DASO_ERR_ARGUMENT, "null buffer or n == 0");
+    if (((uintptr_t(x) | uintptr_t(g) | uintptr_t(v)) & 15u) != 0)
+        return c->fail(DASO_ERR_ARGUMENT, "x, g, v must be 16-byte aligned");
+    const int64_t q = 64 * int64_t(c->G);
+    c->x = x;
+    c->g = g;
+    c->v = v;
+    c->n = int64_t(n);
+    c->n_pad = (int64_t(n) + q - 1) / q * q;
+    c->seg = c->cfg.mode == DASO_MODE_SHARDED ? c->n_pad / c->G : c->n_pad;
+    if (c->P > 1) {
+        const size_t bytes = size_t(c->P) * size_t(c->seg) * c->wire_bytes;
+        CUDA_TRY(c, cudaMalloc(&c->slot, bytes));
+        CUDA_TRY(c, cudaMemset(c->slot, 0, bytes));
+    }
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    c->bound = true;
+    return DASO_OK;
+}
+
+daso_status daso_local_sync(daso_ctx* c, void* stream) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
+    if (c->G > 1)
+        NCCL_TRY(c, ncclAllReduce(c->g, c->g, size_t(c->n), ncclFloat32, ncclSum, c->node_comm,
+                                  static_cast<cudaStream_t>(stream)));
+    return DASO_OK;
+}
+
+daso_status daso_local_update(daso_ctx* c, float lr, void* stream) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
+    KERN_TRY(c, daso::launch_fused(daso::OP_UPDATE, c->cfg.wire, base_args(c, 0, c->n, lr), stream));
+    return DASO_OK;
+}
+
+daso_status daso_global_send(daso_ctx* c, int group, int S, void* stream) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
+    if (c->inflight) return c->fail(DASO_ERR_PROTOCOL, "an exchange is already in flight");
+    if (group < 0 || group >= c->G) return c->fail(DASO_ERR_RANGE, "group %d outside [0, %d)", group, c->G);
+    if (S < 0) return c->fail(DASO_ERR_ARGUMENT, "S must be >= 0");
+    if (c->P == 1) return DASO_OK;   // global tier disabled (R12)
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool member = c->local == group;
+    if (member) {
+        daso::KernelArgs p = base_args(c, 0, c->n, 0.f);
+        p.pack_out = own_segment(c);
+        p.flag = nullptr;
+        KERN_TRY(c, daso::launch_fused(daso::OP_PACK, c->cfg.wire, p, s));
+        STATUS_TRY(start_exchange(c, s));
+    }
+    if (S == 0) {
+        if (member) {
+            STATUS_TRY(wait_exchange(c, s));
+            daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
+            av.den = float(c->P);
+            KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+        }
+        STATUS_TRY(node_bcast(c, group, s));
+    } else {
+        c->inflight = true;
+        c->infl_group = group;
+        c->infl_S = S;
+    }
+    return DASO_OK;
+}
+
+daso_status daso_global_merge(daso_ctx* c, void* stream) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
+    if (!c->inflight) return c->fail(DASO_ERR_PROTOCOL, "no exchange in flight to merge");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (c->local == c->infl_group) {
+        STATUS_TRY(wait_exchange(c, s));
+        daso::KernelArgs m = base_args(c, 0, c->n, 0.f);
+        m.den = float(2 * c->infl_S + c->P);
+        KERN_TRY(c, daso::launch_fused(daso::OP_MERGE, c->cfg.wire, m, s));
+    }
+    STATUS_TRY(node_bcast(c, c->infl_group, s));
+    c->inflight = false;
+    return DASO_OK;
+}
+
+daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    const daso_record r = c->sched->next(plateau);
+    c->last = r;
+    if (out) *out = r;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (r.merge && c->P > 1 && !c->inflight)
+        return c->fail(DASO_ERR_PROTOCOL, "schedule merge at step %lld but nothing in flight", (long long)r.step);
+    if (c->cfg.mode == DASO_MODE_SHARDED) return step_sharded(c, r, lr, s);
+    return step_faithful(c, r, lr, s);
+}
+
+daso_status daso_step_host(daso_ctx* c, const float* host_grads, float lr, int plateau, void* stream,
+                           daso_record* out, uint32_t* host_flag) {
+    if (!c || !host_grads) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(c, cudaMemcpyAsync(c->g, host_grads, size_t(c->n) * sizeof(float), cudaMemcpyHostToDevice, s));
+    STATUS_TRY(daso_step(c, lr, plateau, stream, out));
+    if (host_flag) {
+        CUDA_TRY(c, cudaMemcpyAsync(host_flag, c->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(uint32_t), s));
+    }
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return DASO_OK;
+}
+
+daso_status daso_query(const daso_ctx* c, daso_record* last) {
+    if (!c || !last) return DASO_ERR_ARGUMENT;
+    *last = c->last;
+    return DASO_OK;
+}
+
+daso_status daso_check_finite(daso_ctx* c, void* stream) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    if (!c->d_flag) return c->fail(DASO_ERR_PROTOCOL, "not initialised");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t h = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&h, c->d_flag, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(uint32_t), s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (h) return c->fail(DASO_ERR_NONFINITE, "non-finite parameter written");
+    return DASO_OK;
+}
+
+daso_status daso_topology(const daso_ctx* c, int* P, int* G, int* node, int* local) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    if (P) *P = c->P;
+    if (G) *G = c->G;
+    if (node) *node = c->node;
+    if (local) *local = c->local;
+    return DASO_OK;
+}
+
+daso_status daso_finalize(daso_ctx* c) {
+    if (!c) return DASO_OK;
+    daso_status st = DASO_OK;
+    if (c->side) cudaStreamSynchronize(c->side);   // drain an in-flight exchange
+    cudaDeviceSynchronize();
+    ncclComm_t comms[3] = {c->group_comm, c->node_comm, c->world_comm};
+    for (ncclComm_t m : comms) {
+        if (!m) continue;
+        if (ncclCommFinalize(m) != ncclSuccess) st = DASO_ERR_NCCL;
+        if (ncclCommDestroy(m) != ncclSuccess) st = DASO_ERR_NCCL;
+    }
+    if (c->ev_packed) cudaEventDestroy(c->ev_packed);
+    if (c->ev_exchanged) cudaEventDestroy(c->ev_exchanged);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->slot) cudaFree(c->slot);
+    if (c->d_flag) cudaFree(c->d_flag);
+    delete c->sched;
+    delete c;
+    return st;
+}
+
+const char* daso_last_error(const daso_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+// ---------------------------------------------------------------- kernel entry points
+static bool aligned16(const void* p) { return (uintptr_t(p) & 15u) == 0; }
+
+static daso_status kstatus(int e) { return e == 0 ? DASO_OK : DASO_ERR_CUDA; }
+
+daso_status daso_k_update(float* x, float* v, const float* g, size_t n, float lr, float mu, float wd, float gscale,
+                          void* pack_out, int wire, uint32_t* flag, void* stream) {
+    if (!x || !v || !g || !aligned16(x) || !aligned16(v) || !aligned16(g)) return DASO_ERR_ARGUMENT;
+    if (pack_out && !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
+    if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    daso::KernelArgs a;
+    a.x = x; a.v = v; a.g = g; a.n = int64_t(n);
+    a.lr = lr; a.mu = mu; a.wd = wd; a.gscale = gscale;
+    a.pack_out = pack_out; a.flag = flag;
+    return kstatus(daso::launch_fused(daso::OP_UPDATE | (pack_out ? daso::OP_PACK : 0), wire, a, stream));
+}
+
+static bool slot_ok(const void* slot, size_t stride, int P, int wire) {
+    const size_t eb = wire == DASO_WIRE_BF16 ? 2 : 4;
+    return slot && P >= 1 && aligned16(slot) && (stride * eb) % 16 == 0;
+}
+
+daso_status daso_k_update_merge(float* x, float* v, const float* g, size_t n, float lr, float mu, float wd,
+                                float gscale, const void* slot, size_t slot_stride, int P, int S, void* pack_out,
+                                int wire, uint32_t* flag, void* stream) {
+    if (!x || !v || !g || !aligned16(x) || !aligned16(v) || !aligned16(g)) return DASO_ERR_ARGUMENT;
+    if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n || S < 1) return DASO_ERR_ARGUMENT;
+    if (pack_out && !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
+    daso::KernelArgs a;
+    a.x = x; a.v = v; a.g = g; a.n = int64_t(n);
+    a.lr = lr; a.mu = mu; a.wd = wd; a.gscale = gscale;
+    a.slot = slot; a.slot_stride = int64_t(slot_stride); a.P = P; a.den = float(2 * S + P);
+    a.pack_out = pack_out; a.flag = flag;
+    return kstatus(daso::launch_fused(daso::OP_UPDATE | daso::OP_MERGE | (pack_out ? daso::OP_PACK : 0), wire, a,
+                                      stream));
+}
+
+daso_status daso_k_merge(float* x, size_t n, const void* slot, size_t slot_stride, int P, int S, void* pack_out,
+                         int wire, uint32_t* flag, void* stream) {
+    if (!x || !aligned16(x)) return DASO_ERR_ARGUMENT;
+    if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n || S < 1) return DASO_ERR_ARGUMENT;
+    if (pack_out && !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
+    daso::KernelArgs a;
+    a.x = x; a.n = int64_t(n);
+    a.slot = slot; a.slot_stride = int64_t(slot_stride); a.P = P; a.den = float(2 * S + P);
+    a.pack_out = pack_out; a.flag = flag;
+    return kstatus(daso::launch_fused(daso::OP_MERGE | (pack_out ? daso::OP_PACK : 0), wire, a, stream));
+}
+
+daso_status daso_k_average(float* x, size_t n, const void* slot, size_t slot_stride, int P, int wire, uint32_t* flag,
+                           void* stream) {
+    if (!x || !aligned16(x)) return DASO_ERR_ARGUMENT;
+    if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n) return DASO_ERR_ARGUMENT;
+    daso::KernelArgs a;
+    a.x = x; a.n = int64_t(n);
+    a.slot = slot; a.slot_stride = int64_t(slot_stride); a.P = P; a.den = float(P);
+    a.flag = flag;
+    return kstatus(daso::launch_fused(daso::OP_AVERAGE, wire, a, stream));
+}
+
+daso_status daso_k_pack(const float* x, size_t n, void* pack_out, int wire, void* stream) {
+    if (!x || !pack_out || !aligned16(x) || !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
+    if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    daso::KernelArgs a;
+    a.x = const_cast<float*>(x); a.n = int64_t(n);
+    a.pack_out = pack_out;
+    return kstatus(daso::launch_fused(daso::OP_PACK, wire, a, stream));
+}
+
+daso_status daso_flat_layout(const size_t* numel, int count, size_t align_elems, size_t* offsets, size_t* total) {
+    if (!numel || !offsets || !total || count < 0 || align_elems == 0) return DASO_ERR_ARGUMENT;
+    size_t off = 0;
+    for (int i = 0; i < count; ++i) {
+        offsets[i] = off;
+        off += (numel[i] + align_elems - 1) / align_elems * align_elems;
+    }
+    *total = off;
+    return DASO_OK;
+}
+
+daso_status daso_k_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count, float* dst,
+                          void* stream) {
+    if (!src || !numel || !offsets || !dst || count < 0) return DASO_ERR_ARGUMENT;
+    return kstatus(daso::launch_gather(src, numel, offsets, count, dst, stream));
+}
+
+daso_status daso_k_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets, int count,
+                           void* stream) {
+    if (!src || !numel || !offsets || !dst || count < 0) return DASO_ERR_ARGUMENT;
+    return kstatus(daso::launch_scatter(src, dst, numel, offsets, count, stream));
+}
+
+daso_status daso_k_checksum(const float* x, size_t n, uint64_t* out_dev, void* stream) {
+    if (!x || !out_dev) return DASO_ERR_ARGUMENT;
+    return kstatus(daso::launch_checksum(x, int64_t(n), out_dev, stream));
+}
+
+}  // extern "C"

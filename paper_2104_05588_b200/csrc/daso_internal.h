@@ -1,0 +1,59 @@
+// Internal declarations shared by the translation units of libdaso.so.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "daso.h"
+
+namespace daso {
+
+int resolved_S(const daso_sched_config& c);
+const char* validate_sched(const daso_sched_config& c);   // nullptr = valid
+int phase_of(int64_t epoch, const daso_sched_config& c);
+
+struct Schedule {
+    daso_sched_config cfg;
+    int B = 1, S = 0;
+    int64_t step = 0;
+    int batch_in_cycle = 0;
+    int64_t n_syncs = 0;
+    bool has_pending = false;
+    int64_t pend_due = -1, pend_sent = -1;
+    int pend_S = 0, pend_group = -1;
+
+    explicit Schedule(const daso_sched_config& c);
+    daso_record next(int plateau);
+};
+
+// ---- kernel launchers (kernels.cu); return a cudaError_t as int ----------
+enum Op : int {
+    OP_UPDATE = 1,   // K1
+    OP_MERGE = 2,    // Eq. (1)
+    OP_PACK = 4,     // wire cast into pack_out
+    OP_AVERAGE = 8,  // K4 blocking average
+};
+
+struct KernelArgs {
+    float* x = nullptr;
+    float* v = nullptr;
+    const float* g = nullptr;
+    int64_t n = 0;
+    float lr = 0.f, mu = 0.f, wd = 0.f, gscale = 1.f;
+    const void* slot = nullptr;   // [P][slot_stride] wire elements
+    int64_t slot_stride = 0;
+    int P = 0;
+    float den = 1.f;              // 2S + P (merge) or P (average)
+    void* pack_out = nullptr;
+    uint32_t* flag = nullptr;
+};
+
+int launch_fused(int ops, int wire, const KernelArgs& a, void* stream);
+int launch_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count,
+                  float* dst, void* stream);
+int launch_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets,
+                   int count, void* stream);
+int launch_checksum(const float* x, int64_t n, uint64_t* out, void* stream);
+
+}  // namespace daso
