@@ -173,6 +173,23 @@ daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_rec
 daso_status daso_step_host(daso_ctx* c, const float* host_grads, float lr, int plateau,
                            void* stream, daso_record* out, uint32_t* host_flag);
 
+/* ----- tracing: CUDA events around every phase of daso_step -----
+ * With tracing on, daso_step records an event pair around each phase on the stream
+ * that runs it; daso_trace_read synchronises the ctx's streams and returns the summed
+ * device durations and the algorithmic byte counts since the last reset.
+ * The byte counts are the method's minimum per launch (e.g. K1 = 20 B/param), not
+ * measured DRAM traffic. */
+typedef struct {
+    int64_t steps;
+    int64_t kernel_launches;  double kernel_ms;  double kernel_bytes;  /* fused update/merge/pack/average (HBM) */
+    int64_t local_ops;        double local_ms;   double local_bytes;   /* node all-reduce / reduce-scatter of g (bus bytes) */
+    int64_t node_ops;         double node_ms;    double node_bytes;    /* node broadcast / all-gather of x (bus bytes) */
+    int64_t wait_ops;         double wait_ms;                          /* compute-stream time blocked on the exchange */
+    int64_t exch_ops;         double exch_ms;    double exch_bytes;    /* side-stream group all-gathers (bytes received) */
+} daso_trace;
+daso_status daso_trace_enable(daso_ctx* c, int on);
+daso_status daso_trace_read(daso_ctx* c, daso_trace* out, int reset);
+
 /* Last schedule record and whether an exchange is in flight (host-only, no sync). */
 daso_status daso_query(const daso_ctx* c, daso_record* last);
 /* Synchronise `stream` and read (then clear) the fused non-finite flag:

@@ -44,6 +44,20 @@ class Config(C.Structure):
                 ("check_finite", C.c_int32), ("nccl_max_ctas", C.c_int32)]
 
 
+TRACE_FIELDS = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("kernel_ms", C.c_double),
+                ("kernel_bytes", C.c_double), ("local_ops", C.c_int64), ("local_ms", C.c_double),
+                ("local_bytes", C.c_double), ("node_ops", C.c_int64), ("node_ms", C.c_double),
+                ("node_bytes", C.c_double), ("wait_ops", C.c_int64), ("wait_ms", C.c_double),
+                ("exch_ops", C.c_int64), ("exch_ms", C.c_double), ("exch_bytes", C.c_double)]
+
+
+class Trace(C.Structure):
+    _fields_ = TRACE_FIELDS
+
+    def as_dict(self) -> dict:
+        return {f: (float(getattr(self, f)) if t is C.c_double else int(getattr(self, f))) for f, t in TRACE_FIELDS}
+
+
 class DasoError(RuntimeError):
     def __init__(self, status: int, where: str, msg: str = ""):
         self.status = status
@@ -70,6 +84,8 @@ _SIG = {
     "daso_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_float, C.c_int, C.c_void_p, C.POINTER(Record),
                                  C.POINTER(C.c_uint32)]),
     "daso_query": (C.c_int, [C.c_void_p, C.POINTER(Record)]),
+    "daso_trace_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "daso_trace_read": (C.c_int, [C.c_void_p, C.POINTER(Trace), C.c_int]),
     "daso_check_finite": (C.c_int, [C.c_void_p, C.c_void_p]),
     "daso_finalize": (C.c_int, [C.c_void_p]),
     "daso_last_error": (C.c_char_p, [C.c_void_p]),

@@ -21,6 +21,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "daso_internal.h"
 
@@ -47,6 +48,14 @@ struct daso_ctx {
 
     daso_record last{};
     std::string err;
+
+    // tracing (daso_trace_enable / daso_trace_read)
+    struct SpanRec { cudaEvent_t a, b; int phase; double bytes; };
+    bool tracing = false;
+    std::vector<cudaEvent_t> pool;
+    size_t pool_used = 0;
+    std::vector<SpanRec> spans;
+    daso_trace acc{};
 
     daso_status fail(daso_status s, const char* fmt, ...) {
         char buf[512];
@@ -126,19 +135,70 @@ void* own_segment(daso_ctx* c) {
     return static_cast<char*>(c->slot) + size_t(c->node) * size_t(c->seg) * c->wire_bytes;
 }
 
+// ---- tracing ---------------------------------------------------------------------
+enum Phase { PH_KERNEL = 0, PH_LOCAL = 1, PH_NODE = 2, PH_WAIT = 3, PH_EXCH = 4 };
+
+cudaEvent_t next_event(daso_ctx* c) {
+    if (c->pool_used == c->pool.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->pool.push_back(e);
+    }
+    return c->pool[c->pool_used++];
+}
+
+struct Span {   // RAII event pair around one phase on one stream
+    daso_ctx* c;
+    cudaStream_t s;
+    int phase;
+    double bytes;
+    cudaEvent_t a = nullptr;
+    Span(daso_ctx* c_, cudaStream_t s_, int ph, double b) : c(c_), s(s_), phase(ph), bytes(b) {
+        if (c->tracing && (a = next_event(c)) != nullptr) cudaEventRecord(a, s);
+    }
+    ~Span() {
+        if (!a) return;
+        cudaEvent_t b = next_event(c);
+        if (!b) return;
+        cudaEventRecord(b, s);
+        c->spans.push_back({a, b, phase, bytes});
+    }
+};
+
+// algorithmic HBM bytes per element of a fused launch
+double kernel_bytes_per_elem(int ops, int P, double wb) {
+    double b = 0;
+    if (ops & daso::OP_UPDATE) b += 20;                                  // x, v read+write, g read
+    else if (ops & daso::OP_MERGE) b += 8;                               // x read+write
+    else if (ops & daso::OP_PACK) b += 4;                                // x read
+    if (ops & daso::OP_MERGE) b += P * wb;                               // P slot rows
+    if (ops & daso::OP_AVERAGE) b += P * wb + 4;                         // P slot rows, x write
+    if (ops & daso::OP_PACK) b += wb;                                    // own slot segment
+    return b;
+}
+
+int launch(daso_ctx* c, int ops, const daso::KernelArgs& a, cudaStream_t s) {
+    Span sp(c, s, PH_KERNEL, kernel_bytes_per_elem(ops, a.P, double(c->wire_bytes)) * double(a.n));
+    return daso::launch_fused(ops, c->cfg.wire, a, s);
+}
+
 // ---- collectives ---------------------------------------------------------------
 // Non-blocking global exchange: after the packing kernel on the compute
 // stream, the side stream runs the in-place group all-gather of the slot.
 daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
     CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
-    NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
-                              c->side));
+    {
+        Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(c->seg) * double(c->wire_bytes));
+        NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
+                                  c->side));
+    }
     CUDA_TRY(c, cudaEventRecord(c->ev_exchanged, c->side));
     return DASO_OK;
 }
 
 daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
+    Span sp(c, s, PH_WAIT, 0.0);
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));
     return DASO_OK;
 }
@@ -146,6 +206,7 @@ daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
 // Fig. 4 local update: the group member's parameters replace the node's.
 daso_status node_bcast(daso_ctx* c, int root, cudaStream_t s) {
     if (c->G == 1) return DASO_OK;
+    Span sp(c, s, PH_NODE, 4.0 * double(c->n));
     NCCL_TRY(c, ncclBroadcast(c->x, c->x, size_t(c->n), ncclFloat32, root, c->node_comm, s));
     return DASO_OK;
 }
@@ -153,8 +214,10 @@ daso_status node_bcast(daso_ctx* c, int root, cudaStream_t s) {
 // ---- faithful (v1) batch ---------------------------------------------------------
 daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s) {
     const bool global = c->P > 1;
-    if (c->G > 1)   // Fig. 2: node-local gradient sum (x 1/G in the kernel)
+    if (c->G > 1) {   // Fig. 2: node-local gradient sum (x 1/G in the kernel)
+        Span sp(c, s, PH_LOCAL, 2.0 * (c->G - 1) / c->G * 4.0 * double(c->n));
         NCCL_TRY(c, ncclAllReduce(c->g, c->g, size_t(c->n), ncclFloat32, ncclSum, c->node_comm, s));
+    }
 
     const bool merge = global && r.merge;
     const bool merge_here = merge && c->local == r.merge_group;
@@ -175,7 +238,7 @@ daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStrea
         ops |= daso::OP_PACK;
         a.pack_out = own_segment(c);
     }
-    KERN_TRY(c, daso::launch_fused(ops, c->cfg.wire, a, s));
+    KERN_TRY(c, launch(c, ops, a, s));
     if (merge) {
         STATUS_TRY(node_bcast(c, int(r.merge_group), s));
         c->inflight = false;
@@ -184,7 +247,7 @@ daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStrea
         daso::KernelArgs p = base_args(c, 0, c->n, 0.f);
         p.pack_out = own_segment(c);
         p.flag = nullptr;
-        KERN_TRY(c, daso::launch_fused(daso::OP_PACK, c->cfg.wire, p, s));
+        KERN_TRY(c, launch(c, daso::OP_PACK, p, s));
     }
     if (send) {
         if (send_here) STATUS_TRY(start_exchange(c, s));
@@ -193,7 +256,7 @@ daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStrea
                 STATUS_TRY(wait_exchange(c, s));
                 daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
                 av.den = float(c->P);
-                KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+                KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
             }
             STATUS_TRY(node_bcast(c, int(r.send_group), s));
         } else {
@@ -213,8 +276,10 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
     const bool global = c->P > 1;
     const int64_t sh = c->seg;
     const int64_t off = int64_t(c->local) * sh;
-    if (c->G > 1)
+    if (c->G > 1) {
+        Span sp(c, s, PH_LOCAL, double(c->G - 1) / c->G * 4.0 * double(c->n_pad));
         NCCL_TRY(c, ncclReduceScatter(c->g, c->g + off, size_t(sh), ncclFloat32, ncclSum, c->node_comm, s));
+    }
     const bool merge = global && r.merge;
     const bool send = global && r.send;
     daso::KernelArgs a = base_args(c, off, sh, lr);
@@ -229,22 +294,24 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
         ops |= daso::OP_PACK;
         a.pack_out = own_segment(c);
     }
-    KERN_TRY(c, daso::launch_fused(ops, c->cfg.wire, a, s));
+    KERN_TRY(c, launch(c, ops, a, s));
     if (send) {
         STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {
             STATUS_TRY(wait_exchange(c, s));
             daso::KernelArgs av = base_args(c, off, sh, 0.f);
             av.den = float(c->P);
-            KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+            KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
         } else {
             c->inflight = true;
             c->infl_group = int(r.send_group);
             c->infl_S = int(r.S);
         }
     }
-    if (c->G > 1)
+    if (c->G > 1) {
+        Span sp(c, s, PH_NODE, double(c->G - 1) / c->G * 4.0 * double(c->n_pad));
         NCCL_TRY(c, ncclAllGather(c->x + off, c->x, size_t(sh), ncclFloat32, c->node_comm, s));
+    }
     return DASO_OK;
 }
 
@@ -368,9 +435,11 @@ daso_status daso_local_sync(daso_ctx* c, void* stream) {
     if (!c) return DASO_ERR_ARGUMENT;
     STATUS_TRY(require_bound(c));
     if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
-    if (c->G > 1)
+    if (c->G > 1) {
+        Span sp(c, static_cast<cudaStream_t>(stream), PH_LOCAL, 2.0 * (c->G - 1) / c->G * 4.0 * double(c->n));
         NCCL_TRY(c, ncclAllReduce(c->g, c->g, size_t(c->n), ncclFloat32, ncclSum, c->node_comm,
                                   static_cast<cudaStream_t>(stream)));
+    }
     return DASO_OK;
 }
 
@@ -378,7 +447,7 @@ daso_status daso_local_update(daso_ctx* c, float lr, void* stream) {
     if (!c) return DASO_ERR_ARGUMENT;
     STATUS_TRY(require_bound(c));
     if (c->cfg.mode != DASO_MODE_FAITHFUL) return c->fail(DASO_ERR_PROTOCOL, "split API requires DASO_MODE_FAITHFUL");
-    KERN_TRY(c, daso::launch_fused(daso::OP_UPDATE, c->cfg.wire, base_args(c, 0, c->n, lr), stream));
+    KERN_TRY(c, launch(c, daso::OP_UPDATE, base_args(c, 0, c->n, lr), static_cast<cudaStream_t>(stream)));
     return DASO_OK;
 }
 
@@ -396,7 +465,7 @@ daso_status daso_global_send(daso_ctx* c, int group, int S, void* stream) {
         daso::KernelArgs p = base_args(c, 0, c->n, 0.f);
         p.pack_out = own_segment(c);
         p.flag = nullptr;
-        KERN_TRY(c, daso::launch_fused(daso::OP_PACK, c->cfg.wire, p, s));
+        KERN_TRY(c, launch(c, daso::OP_PACK, p, s));
         STATUS_TRY(start_exchange(c, s));
     }
     if (S == 0) {
@@ -404,7 +473,7 @@ daso_status daso_global_send(daso_ctx* c, int group, int S, void* stream) {
             STATUS_TRY(wait_exchange(c, s));
             daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
             av.den = float(c->P);
-            KERN_TRY(c, daso::launch_fused(daso::OP_AVERAGE, c->cfg.wire, av, s));
+            KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
         }
         STATUS_TRY(node_bcast(c, group, s));
     } else {
@@ -425,7 +494,7 @@ daso_status daso_global_merge(daso_ctx* c, void* stream) {
         STATUS_TRY(wait_exchange(c, s));
         daso::KernelArgs m = base_args(c, 0, c->n, 0.f);
         m.den = float(2 * c->infl_S + c->P);
-        KERN_TRY(c, daso::launch_fused(daso::OP_MERGE, c->cfg.wire, m, s));
+        KERN_TRY(c, launch(c, daso::OP_MERGE, m, s));
     }
     STATUS_TRY(node_bcast(c, c->infl_group, s));
     c->inflight = false;
@@ -437,6 +506,7 @@ daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_rec
     STATUS_TRY(require_bound(c));
     const daso_record r = c->sched->next(plateau);
     c->last = r;
+    if (c->tracing) c->acc.steps += 1;
     if (out) *out = r;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (r.merge && c->P > 1 && !c->inflight)
@@ -457,6 +527,33 @@ daso_status daso_step_host(daso_ctx* c, const float* host_grads, float lr, int p
         CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(uint32_t), s));
     }
     CUDA_TRY(c, cudaStreamSynchronize(s));
+    return DASO_OK;
+}
+
+daso_status daso_trace_enable(daso_ctx* c, int on) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    c->tracing = on != 0;
+    return DASO_OK;
+}
+
+daso_status daso_trace_read(daso_ctx* c, daso_trace* out, int reset) {
+    if (!c || !out) return DASO_ERR_ARGUMENT;
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    for (const auto& sp : c->spans) {
+        float ms = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&ms, sp.a, sp.b));
+        switch (sp.phase) {
+            case PH_KERNEL: c->acc.kernel_launches++; c->acc.kernel_ms += ms; c->acc.kernel_bytes += sp.bytes; break;
+            case PH_LOCAL: c->acc.local_ops++; c->acc.local_ms += ms; c->acc.local_bytes += sp.bytes; break;
+            case PH_NODE: c->acc.node_ops++; c->acc.node_ms += ms; c->acc.node_bytes += sp.bytes; break;
+            case PH_WAIT: c->acc.wait_ops++; c->acc.wait_ms += ms; break;
+            case PH_EXCH: c->acc.exch_ops++; c->acc.exch_ms += ms; c->acc.exch_bytes += sp.bytes; break;
+        }
+    }
+    c->spans.clear();
+    c->pool_used = 0;
+    *out = c->acc;
+    if (reset) c->acc = daso_trace{};
     return DASO_OK;
 }
 
@@ -498,6 +595,7 @@ daso_status daso_finalize(daso_ctx* c) {
         if (ncclCommFinalize(m) != ncclSuccess) st = DASO_ERR_NCCL;
         if (ncclCommDestroy(m) != ncclSuccess) st = DASO_ERR_NCCL;
     }
+    for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
     if (c->ev_packed) cudaEventDestroy(c->ev_packed);
     if (c->ev_exchanged) cudaEventDestroy(c->ev_exchanged);
     if (c->side) cudaStreamDestroy(c->side);

@@ -139,6 +139,14 @@ class Ctx:
                                          C.byref(r), C.byref(flag)), "daso_step_host")
         return r.as_dict(), int(flag.value)
 
+    def trace_enable(self, on: bool = True):
+        self._check(lib().daso_trace_enable(self._h, int(on)), "daso_trace_enable")
+
+    def trace_read(self, reset: bool = True) -> dict:
+        t = L.Trace()
+        self._check(lib().daso_trace_read(self._h, C.byref(t), int(reset)), "daso_trace_read")
+        return t.as_dict()
+
     def query(self) -> dict:
         r = Record()
         self._check(lib().daso_query(self._h, C.byref(r)), "daso_query")

@@ -1,0 +1,160 @@
+"""End-to-end parity of the whole DASO path on real GPUs (one process per GPU,
+NCCL over NVLink) against the CPU oracle, on the toy config of SURVEY §8(d):
+linear regression d = 1000, per-rank batch 32, 20 steps, seeded data.
+
+Checked every step, on every rank:
+  * parameters vs the oracle: ||gpu - oracle|| / ||oracle|| and elementwise
+    |gpu - oracle| <= tol * (|x_o| + rms(x_o)), tol = 1e-5 (fp32 wire) / 1e-2
+    (bf16 wire) — the north star's bounds;
+  * the schedule record (phase, B, S, send, merge, S_p, groups, ...) bit-exact;
+  * node replicas bitwise identical (order-independent checksum, Fig. 4 invariant).
+World sizes above the visible GPU count are skipped (gpurun grants 1, 2 or 4).
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import synthetic  # noqa: E402
+from oracle import daso_sim, toy  # noqa: E402
+from oracle.schedule import SchedConfig  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_world(tmp, world, args):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
+    out = os.path.join(tmp, "out")
+    if world == 1:
+        sys.path.insert(0, HERE)
+        import mp_toy
+        a = mp_toy.parse([*args, "--out", out])
+        run_torch_single(mp_toy, a)
+    else:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_toy.py"),
+               *args, "--out", out]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    return [np.load(os.path.join(out, f"rank{i}.npz")) for i in range(world)]
+
+
+def run_torch_single(mp_toy, a):
+    torch.cuda.set_device(0)
+    mp_toy.run_toy(a, 0, 1)
+
+
+def check(ranks, P, G, B, S, steps=20, d=1000, b=32, lr=0.01, mu=0.9, wd=1e-4, wire="bf16", warm=0, cool=0,
+          epochs=1, spe=20, flags=""):
+    cache = {}
+
+    def grad_fn(r, k, w):
+        if (r, k) not in cache:
+            cache[(r, k)] = synthetic.toy_batch(d, b, r, k)
+        return toy.grad(w, *cache[(r, k)])
+
+    cfg = SchedConfig(B_init=B, S_init=S, warmup_epochs=warm, cooldown_epochs=cool, total_epochs=epochs,
+                      steps_per_epoch=spe)
+    ref = daso_sim.simulate(P, G, cfg, steps, np.zeros(d), grad_fn, lr, mu, wd, wire=wire,
+                            epoch_flags=[int(c) for c in flags], trace=True)
+    tol = 1e-2 if wire == "bf16" else 1e-5
+    worst = 0.0
+    for r, f in enumerate(ranks):
+        tr = f["trace"].astype(np.float64)
+        for k in range(steps):
+            xo = ref["trace"][k][r]
+            rms = np.sqrt(np.mean(xo ** 2))
+            err = np.abs(tr[k] - xo)
+            assert np.all(err <= tol * (np.abs(xo) + rms)), (r, k, float(np.max(err / (np.abs(xo) + rms))))
+            rel = np.linalg.norm(tr[k] - xo) / max(np.linalg.norm(xo), 1e-30)
+            assert rel <= tol, (r, k, rel)
+            worst = max(worst, rel)
+        fields = [str(s) for s in f["rec_fields"]]
+        for k in range(steps):
+            got = dict(zip(fields, (int(v) for v in f["recs"][k])))
+            assert got == ref["records"][k].as_dict(), (r, k, got, ref["records"][k].as_dict())
+    for j in range(P):   # node replicas bitwise identical, every step
+        for l in range(1, G):
+            np.testing.assert_array_equal(ranks[j * G + l]["cks"], ranks[j * G]["cks"])
+    return worst
+
+
+TOY = ["--B", "4", "--S", "1"]
+
+
+@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+def test_world1_is_plain_sgd(tmp_path, mode):
+    ranks = run_world(str(tmp_path), 1, TOY + ["--P", "1", "--G", "1", "--mode", mode, "--wire", "fp32"])
+    check(ranks, 1, 1, 4, 1, wire="fp32")
+
+
+@pytest.mark.parametrize("P,G", [(2, 1), (1, 2)])
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+def test_world2_toy(tmp_path, P, G, wire):
+    ranks = run_world(str(tmp_path), 2, TOY + ["--P", str(P), "--G", str(G), "--wire", wire])
+    check(ranks, P, G, 4, 1, wire=wire)
+
+
+def test_world2_scheduled_with_plateaus(tmp_path):
+    args = ["--P", "2", "--G", "1", "--B", "4", "--S", "2", "--warmup", "1", "--cooldown", "1", "--epochs", "6",
+            "--spe", "4", "--steps", "24", "--flags", "011010"]
+    ranks = run_world(str(tmp_path), 2, args)
+    check(ranks, 2, 1, 4, 2, steps=24, warm=1, cool=1, epochs=6, spe=4, flags="011010")
+
+
+def test_world2_S_equals_B(tmp_path):
+    ranks = run_world(str(tmp_path), 2, ["--P", "2", "--G", "1", "--B", "2", "--S", "2", "--wire", "fp32"])
+    check(ranks, 2, 1, 2, 2, wire="fp32")
+
+
+def test_world2_blocking_fp32_is_flat_sync(tmp_path):
+    """B=1, S=0, fp32 wire: DASO == synchronous SGD over the concatenated batch."""
+    ranks = run_world(str(tmp_path), 2, ["--P", "2", "--G", "1", "--B", "1", "--S", "0", "--wire", "fp32"])
+    check(ranks, 2, 1, 1, 0, wire="fp32")
+    np.testing.assert_array_equal(ranks[0]["cks"], ranks[1]["cks"])   # blocking: all ranks identical
+
+
+@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+def test_world4_toy_config1(tmp_path, mode, wire):
+    """Config 1 proper: 2 virtual nodes x 2 GPUs, B=4, S=1, 20 steps."""
+    ranks = run_world(str(tmp_path), 4, TOY + ["--P", "2", "--G", "2", "--mode", mode, "--wire", wire])
+    check(ranks, 2, 2, 4, 1, wire=wire)
+
+
+def test_world4_split_api_equals_step(tmp_path):
+    a = run_world(str(tmp_path / "a"), 4, TOY + ["--P", "2", "--G", "2"])
+    b = run_world(str(tmp_path / "b"), 4, TOY + ["--P", "2", "--G", "2", "--split"])
+    for ra, rb in zip(a, b):
+        np.testing.assert_array_equal(ra["trace"].view(np.uint32), rb["trace"].view(np.uint32))
+
+
+@pytest.mark.parametrize("P,G", [(4, 1), (1, 4)])
+def test_world4_other_topologies(tmp_path, P, G):
+    ranks = run_world(str(tmp_path), 4, TOY + ["--P", str(P), "--G", str(G)])
+    check(ranks, P, G, 4, 1)
+
+
+@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+def test_world4_full_schedule(tmp_path, mode):
+    args = ["--P", "2", "--G", "2", "--B", "4", "--S", "1", "--warmup", "1", "--cooldown", "1", "--epochs", "5",
+            "--spe", "8", "--steps", "40", "--flags", "01100", "--mode", mode]
+    ranks = run_world(str(tmp_path), 4, args)
+    check(ranks, 2, 2, 4, 1, steps=40, warm=1, cool=1, epochs=5, spe=8, flags="01100")
