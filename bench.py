@@ -159,8 +159,7 @@ def barrier(world):
 
 def cpu_baseline(P, G, B, S, n, wire):
     from oracle import bench as obench
-    n_sample = max(1 << 16, n // 16)
-    r = obench.calibrated(P, G, B, S, n_sample, budget_s=12.0, wire=wire)
+    r = obench.calibrated(P, G, B, S, n, budget_s=12.0, wire=wire)
     gbs = 4.0 * r["n"] * r["ranks"] / r["s_per_step"] / 1e9
     return {"value": gbs, "unit": "GB/s", "cores": r["cores"], "kind": "oracle",
             "ms_per_step": r["s_per_step"] * 1e3 * (n / r["n"]),

@@ -51,5 +51,5 @@ def calibrated(P: int, G: int, B: int, S: int, n_sample: int, budget_s: float = 
     x0 = synthetic.microbench_x0(n_sample)
     grads = [synthetic.microbench_grad(n_sample, r, 0) for r in range(P * G)]
     probe = time_sync_path(P, G, B, S, n_sample, 1, x0=x0, grads=grads, wire=wire)
-    steps = int(max(2, min(200, budget_s / max(probe["s_per_step"], 1e-6))))
+    steps = int(max(2, min(2000, budget_s / max(probe["s_per_step"], 1e-6))))
     return time_sync_path(P, G, B, S, n_sample, steps, x0=x0, grads=grads, wire=wire)

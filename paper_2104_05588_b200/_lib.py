@@ -108,6 +108,7 @@ _SIG = {
     "daso_k_scatter": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t),
                                  C.c_int, C.c_void_p]),
     "daso_k_checksum": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
+    "daso_kernel_impl": (C.c_int, [C.c_int]),
 }
 EXPORTED = sorted(_SIG)
 

@@ -703,6 +703,8 @@ daso_status daso_k_scatter(const float* src, float* const* dst, const size_t* nu
     return kstatus(daso::launch_scatter(src, dst, numel, offsets, count, stream));
 }
 
+int daso_kernel_impl(int impl) { return daso::set_kernel_impl(impl); }
+
 daso_status daso_k_checksum(const float* x, size_t n, uint64_t* out_dev, void* stream) {
     if (!x || !out_dev) return DASO_ERR_ARGUMENT;
     return kstatus(daso::launch_checksum(x, int64_t(n), out_dev, stream));

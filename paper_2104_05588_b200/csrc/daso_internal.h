@@ -50,6 +50,7 @@ struct KernelArgs {
 };
 
 int launch_fused(int ops, int wire, const KernelArgs& a, void* stream);
+int set_kernel_impl(int impl);   // returns the previous selection
 int launch_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count,
                   float* dst, void* stream);
 int launch_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets,

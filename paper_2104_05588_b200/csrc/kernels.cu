@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "daso_internal.h"
 
 namespace daso {
@@ -86,6 +89,20 @@ struct Wire<DASO_WIRE_BF16> {
             for (int j = 0; j < N; ++j) p[j] = __bfloat16_as_ushort(__float2bfloat16_rn(r[j]));
         }
     }
+    template <int N>
+    static __device__ __forceinline__ void load_smem(const void* base, int i, float (&r)[N]) {
+        static_assert(N == 8, "");
+        uint4 u = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(base) + i);
+        r[0] = bf16lo(u.x); r[1] = bf16hi(u.x); r[2] = bf16lo(u.y); r[3] = bf16hi(u.y);
+        r[4] = bf16lo(u.z); r[5] = bf16hi(u.z); r[6] = bf16lo(u.w); r[7] = bf16hi(u.w);
+    }
+    template <int N>
+    static __device__ __forceinline__ void store_smem(void* base, int i, const float (&r)[N]) {
+        static_assert(N == 8, "");
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(base) + i) =
+            make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]), pack_bf16x2(r[4], r[5]),
+                       pack_bf16x2(r[6], r[7]));
+    }
 };
 
 template <>
@@ -97,6 +114,20 @@ struct Wire<DASO_WIRE_FP32> {
     template <int N>
     static __device__ __forceinline__ void store(void* base, int64_t i, const float (&r)[N]) {
         st_f32<N>(static_cast<float*>(base) + i, r);
+    }
+    template <int N>
+    static __device__ __forceinline__ void load_smem(const void* base, int i, float (&r)[N]) {
+#pragma unroll
+        for (int j = 0; j < N; j += 4) {
+            float4 q = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + i + j);
+            r[j] = q.x; r[j + 1] = q.y; r[j + 2] = q.z; r[j + 3] = q.w;
+        }
+    }
+    template <int N>
+    static __device__ __forceinline__ void store_smem(void* base, int i, const float (&r)[N]) {
+#pragma unroll
+        for (int j = 0; j < N; j += 4)
+            *reinterpret_cast<float4*>(static_cast<float*>(base) + i + j) = make_float4(r[j], r[j + 1], r[j + 2], r[j + 3]);
     }
 };
 
@@ -169,6 +200,180 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
     }
 }
 
+
+// ----------------------------------------------------------------- TMA-staged variant
+// The same K1/K2/K3 arithmetic with the streams staged through shared memory by the
+// bulk-copy engine (cp.async.bulk, 1-D TMA): one persistent CTA per SM walks its tiles
+// (tile = blockIdx.x + k * gridDim.x) through an NS-deep ring of stages; one elected
+// thread issues the global->shared copies (completion counted in bytes on an mbarrier)
+// and the shared->global stores of x, v and the packed row (bulk_group), all threads
+// compute from shared memory.  NS-1 tiles of loads are in flight per SM while one is
+// computed.  Ragged tail (< kTile elements) falls back to the register path.
+constexpr int kTile = 2048;          // parameters per tile: 8 per thread
+constexpr int kTmaThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct TmaLayout {   // byte offsets inside one stage
+    uint32_t x, v, g, slot, pack, bytes;
+};
+__host__ __device__ inline TmaLayout tma_layout(int ops, int P, int wb) {
+    TmaLayout L{};
+    uint32_t o = 0;
+    L.x = o; o += kTile * 4;
+    L.v = o; o += kTile * 4;
+    L.g = o; o += kTile * 4;
+    L.slot = o; if (ops & OP_MERGE) o += uint32_t(P) * kTile * wb;
+    L.pack = o; if (ops & OP_PACK) o += kTile * wb;
+    L.bytes = (o + 127) / 128 * 128;
+    return L;
+}
+
+template <int OPS, int WIRE>
+__global__ void __launch_bounds__(kTmaThreads, 1) tma_kernel(const KernelArgs a, int NS) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const TmaLayout L = tma_layout(OPS, a.P, wb);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * L.bytes);
+    const int64_t ntiles = a.n / kTile;
+    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const bool leader = threadIdx.x == 0;
+    if (leader) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue_load = [&](int64_t k) {
+        const int s = int(k % NS);
+        unsigned char* st = smem + size_t(s) * L.bytes;
+        const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kTile;
+        uint32_t tx = 3u * kTile * 4u;
+        if constexpr ((OPS & OP_MERGE) != 0) tx += uint32_t(a.P) * kTile * wb;
+        mbar_expect_tx(&full[s], tx);
+        bulk_g2s(st + L.x, a.x + e0, kTile * 4, &full[s]);
+        bulk_g2s(st + L.v, a.v + e0, kTile * 4, &full[s]);
+        bulk_g2s(st + L.g, a.g + e0, kTile * 4, &full[s]);
+        if constexpr ((OPS & OP_MERGE) != 0) {
+            for (int p = 0; p < a.P; ++p)
+                bulk_g2s(st + L.slot + uint32_t(p) * kTile * wb,
+                         static_cast<const unsigned char*>(a.slot) + (p * a.slot_stride + e0) * wb, kTile * wb,
+                         &full[s]);
+        }
+    };
+
+    if (leader)
+        for (int64_t k = 0; k < my && k < NS; ++k) issue_load(k);
+
+    bool bad = false;
+    for (int64_t k = 0; k < my; ++k) {
+        const int s = int(k % NS);
+        unsigned char* st = smem + size_t(s) * L.bytes;
+        mbar_wait(&full[s], uint32_t((k / NS) & 1));
+        const int i = threadIdx.x * kVec;
+        float* xs = reinterpret_cast<float*>(st + L.x) + i;
+        float* vs = reinterpret_cast<float*>(st + L.v) + i;
+        const float* gs = reinterpret_cast<const float*>(st + L.g) + i;
+        float x[kVec], v[kVec], g[kVec];
+#pragma unroll
+        for (int j = 0; j < kVec; j += 4) {
+            float4 a4 = *reinterpret_cast<float4*>(xs + j), b4 = *reinterpret_cast<float4*>(vs + j),
+                   c4 = *reinterpret_cast<const float4*>(gs + j);
+            x[j] = a4.x; x[j + 1] = a4.y; x[j + 2] = a4.z; x[j + 3] = a4.w;
+            v[j] = b4.x; v[j + 1] = b4.y; v[j + 2] = b4.z; v[j + 3] = b4.w;
+            g[j] = c4.x; g[j + 1] = c4.y; g[j + 2] = c4.z; g[j + 3] = c4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+            const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
+            v[j] = fmaf(a.mu, v[j], d);
+            x[j] = fmaf(-a.lr, v[j], x[j]);
+        }
+        if constexpr ((OPS & OP_MERGE) != 0) {
+            float acc[kVec];
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) acc[j] = 0.f;
+            for (int p = 0; p < a.P; ++p) {
+                float sv[kVec];
+                Wire<WIRE>::template load_smem<kVec>(st + L.slot + uint32_t(p) * kTile * wb, i, sv);
+#pragma unroll
+                for (int j = 0; j < kVec; ++j) acc[j] += sv[j] - x[j];
+            }
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) x[j] = x[j] + acc[j] / a.den;
+        }
+#pragma unroll
+        for (int j = 0; j < kVec; j += 4) {
+            *reinterpret_cast<float4*>(xs + j) = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+            *reinterpret_cast<float4*>(vs + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) bad |= !isfinite(x[j]);
+        if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<kVec>(st + L.pack, i, x);
+        fence_async_smem();
+        __syncthreads();
+        if (leader) {
+            const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kTile;
+            bulk_s2g(a.x + e0, st + L.x, kTile * 4);
+            bulk_s2g(a.v + e0, st + L.v, kTile * 4);
+            if constexpr ((OPS & OP_PACK) != 0)
+                bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, st + L.pack, kTile * wb);
+            bulk_commit();
+            if (k >= 1 && k - 1 + NS < my) {   // stage of tile k-1 is free once its stores have read it
+                bulk_wait_read<1>();
+                issue_load(k - 1 + NS);
+            }
+        }
+    }
+    if (leader) bulk_wait_all();
+    if (blockIdx.x == gridDim.x - 1) {   // ragged tail through the register path
+        for (int64_t e = ntiles * kTile + threadIdx.x; e < a.n; e += blockDim.x) body<OPS, WIRE, 1>(a, e, bad);
+    }
+    if (a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
+    }
+}
+
 // ----------------------------------------------------------------- launch config
 struct DevInfo {
     int sms = 0;
@@ -201,8 +406,51 @@ int launch_t(const KernelArgs& a, cudaStream_t s) {
     return int(cudaGetLastError());
 }
 
+int g_impl = -1;   // 0 = register (LDG) path, 1 = TMA-staged path; default from DASO_KERNEL=ldg|tma
+
+int kernel_impl() {
+    if (g_impl < 0) {
+        const char* e = getenv("DASO_KERNEL");
+        g_impl = (e && strcmp(e, "tma") == 0) ? 1 : 0;
+    }
+    return g_impl;
+}
+
+template <int OPS, int WIRE>
+int launch_tma(const KernelArgs& a, cudaStream_t s) {
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const TmaLayout L = tma_layout(OPS, a.P, wb);
+    const int budget = 200 * 1024;
+    int NS = int(std::min<int64_t>(8, (budget - 64) / L.bytes));
+    if (NS < 2) return launch_t<OPS, WIRE>(a, s);
+    const size_t smem = size_t(NS) * L.bytes + 8 * size_t(NS);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tma_kernel<OPS, WIRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    tma_kernel<OPS, WIRE><<<dim3(unsigned(sm_count())), dim3(kTmaThreads), smem, s>>>(a, NS);
+    return int(cudaGetLastError());
+}
+
+bool tma_ok(const KernelArgs& a, int wb) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    return a.n >= kTile && al(a.x) && al(a.v) && al(a.g) && (a.pack_out == nullptr || al(a.pack_out)) &&
+           (a.slot == nullptr || (al(a.slot) && (a.slot_stride * wb) % 16 == 0)) && a.P <= 16;
+}
+
 template <int WIRE>
 int dispatch(int ops, const KernelArgs& a, cudaStream_t s) {
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    if (kernel_impl() == 1 && tma_ok(a, wb)) {
+        switch (ops) {
+            case OP_UPDATE: return launch_tma<OP_UPDATE, WIRE>(a, s);
+            case OP_UPDATE | OP_PACK: return launch_tma<OP_UPDATE | OP_PACK, WIRE>(a, s);
+            case OP_UPDATE | OP_MERGE: return launch_tma<OP_UPDATE | OP_MERGE, WIRE>(a, s);
+            case OP_UPDATE | OP_MERGE | OP_PACK: return launch_tma<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(a, s);
+            default: break;
+        }
+    }
     switch (ops) {
         case OP_UPDATE: return launch_t<OP_UPDATE, WIRE>(a, s);
         case OP_UPDATE | OP_PACK: return launch_t<OP_UPDATE | OP_PACK, WIRE>(a, s);
@@ -281,6 +529,12 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint32_t* __re
 }
 
 }  // namespace
+
+int set_kernel_impl(int impl) {
+    const int prev = kernel_impl();
+    if (impl == 0 || impl == 1) g_impl = impl;
+    return prev;
+}
 
 int launch_fused(int ops, int wire, const KernelArgs& a, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);

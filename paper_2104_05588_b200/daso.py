@@ -268,6 +268,12 @@ def daso_k_scatter(src, tensors, offsets, stream=None):
     check(lib().daso_k_scatter(_ptr(src), dst, numel, offs, n, _stream(stream)), "daso_k_scatter")
 
 
+def daso_kernel_impl(impl: int | str | None = None) -> int:
+    """Select the fused-kernel data path: 0/"ldg" or 1/"tma"; returns the previous one."""
+    code = {"ldg": 0, "tma": 1, None: -1}.get(impl, impl)
+    return int(lib().daso_kernel_impl(int(code)))
+
+
 def daso_k_checksum(x, out_u64, stream=None):
     """out_u64: a 1-element int64 CUDA tensor receiving the checksum bits."""
     check(lib().daso_k_checksum(_ptr(x), x.numel(), _ptr(out_u64), _stream(stream)), "daso_k_checksum")

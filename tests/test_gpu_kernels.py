@@ -129,10 +129,11 @@ def test_k3_update_merge_fp32_wire(n, P, S):
 def test_merge_fixed_point_is_bitwise():
     """Eq. (1) fixed point: identical stale inputs leave x unchanged, bit for bit
     (the delta form x + sum(s - x)/(2S+P) with s == x adds exactly zero)."""
-    n = 4099
+    n, stride = 4099, 4160
     x = synthetic.microbench_x0(n, seed=5)
     X = cuda(x)
-    rows = np.stack([x, x, x]).astype(np.float32)
+    rows = np.zeros((3, stride), np.float32)
+    rows[:, :n] = x
     daso.daso_k_merge(X, cuda(rows), 2, wire="fp32")
     np.testing.assert_array_equal(X.cpu().numpy().view(np.uint32), x.view(np.uint32))
 
@@ -233,3 +234,38 @@ def test_full_size_k3_sampled(P):
     close(V[ti].cpu().numpy(), vo)
     np.testing.assert_array_equal(bits_bf16(out[ti]), expect_bf16_bits(xg))
     assert torch.isfinite(X).all()
+
+
+@pytest.mark.parametrize("n", [2048, 2048 * 37 + 5, 3 * 2 ** 16 + 5, N_FULL])
+@pytest.mark.parametrize("ops", ["K1", "K2", "K3", "K3pack"])
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+def test_tma_path_bit_identical_to_register_path(n, ops, wire):
+    """The TMA-staged data path (daso_kernel_impl(1)) computes the same arithmetic in the
+    same order as the register path: x, v and the packed row must agree bit for bit;
+    the register path itself is pinned to the oracle above."""
+    P, S = 3, 1
+    stride = (n + 511) // 512 * 512
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    base = [torch.randn(n, device="cuda", generator=gen) * s for s in (0.02, 0.01, 0.01)]
+    wdt = torch.bfloat16 if wire == "bf16" else torch.float32
+    slot = (torch.randn(P, stride, device="cuda", generator=gen) * 0.02).to(wdt)
+    outs = []
+    for impl in ("ldg", "tma"):
+        prev = daso.daso_kernel_impl(impl)
+        try:
+            X, V, Gd = (t.clone() for t in base)
+            pk = torch.zeros(stride, dtype=wdt, device="cuda") if ops in ("K2", "K3pack") else None
+            if ops in ("K1", "K2"):
+                daso.daso_k_update(X, V, Gd, 0.1, 0.9, 1e-4, 0.5, pack_out=pk, wire=wire)
+            else:
+                daso.daso_k_update_merge(X, V, Gd, 0.1, 0.9, 1e-4, 0.5, slot, S, pack_out=pk, wire=wire)
+            torch.cuda.synchronize()
+            outs.append((X, V, pk))
+        finally:
+            daso.daso_kernel_impl(prev)
+    (x1, v1, p1), (x2, v2, p2) = outs
+    assert torch.equal(x1.view(torch.int32), x2.view(torch.int32))
+    assert torch.equal(v1.view(torch.int32), v2.view(torch.int32))
+    if p1 is not None:
+        assert torch.equal(p1[:n].view(torch.int16 if wire == "bf16" else torch.int32),
+                           p2[:n].view(torch.int16 if wire == "bf16" else torch.int32))
