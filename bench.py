@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--S", type=int, default=1)
     ap.add_argument("--n", type=int, default=N_PARAMS)
     ap.add_argument("--topology", default="", help="PxG, default by --gpus")
-    ap.add_argument("--mode", choices=["faithful", "sharded"], default="faithful")
+    ap.add_argument("--mode", choices=["faithful", "sharded", "fused"], default="faithful")
     ap.add_argument("--wire", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -250,6 +250,19 @@ def run_ours(a):
                 "kernel": "fused_kernel (K1/K2/K3: update [+merge] [+bf16 pack])",
                 "bytes_per_launch": tr["kernel_bytes"] / max(tr["kernel_launches"], 1),
                 "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1), "peak_source": peak_src}
+    if a.mode == "fused" and G > 1:
+        # the fused node-tier kernel is NVLink-bound: (G-1)/G * 4n bytes leave and enter each GPU
+        nvl_bytes = (G - 1) * 4.0 * daso.daso_padded_numel(n, G) / G
+        nvl_gbs = nvl_bytes / (tr["kernel_ms"] / max(tr["kernel_launches"], 1) * 1e-3) / 1e9
+        nvl_gbs = -max_over_ranks(-nvl_gbs, world)
+        roofline = {"bound": "nvlink", "achieved": nvl_gbs, "peak": 770.0, "unit": "GB/s",
+                    "frac": nvl_gbs / 770.0, "traffic": None,
+                    "kernel": "peer_kernel (node gradient reduce over NVLink + update [+merge] [+pack] + "
+                              "parameter all-gather by NVLink stores)",
+                    "bytes_per_launch": nvl_bytes, "bytes_def": "NVLink bytes per direction per GPU",
+                    "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1),
+                    "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
+                    "hbm": roofline}
     phases = {k: (tr[k] / a.steps if k.endswith("_ms") else tr[k]) for k in tr}
     if tr["local_ms"] > 0:
         phases["local_busbw_gbs"] = tr["local_bytes"] / (tr["local_ms"] * 1e-3) / 1e9

@@ -46,8 +46,12 @@ typedef enum {
 enum { DASO_WARMUP = 0, DASO_CYCLING = 1, DASO_COOLDOWN = 2 };   /* P:97 phases            */
 enum { DASO_WIRE_BF16 = 0, DASO_WIRE_FP32 = 1 };                 /* P:86 / P:88, reading R3 */
 enum { DASO_MODE_FAITHFUL = 0,  /* v1: rotating group exchange + node broadcast (Fig. 4)   */
-       DASO_MODE_SHARDED = 1 }; /* v2: node reduce-scatter, shard update, all groups exchange
-                                   their shard, node all-gather; numerically the same (DESIGN §5) */
+       DASO_MODE_SHARDED = 1,   /* v2: node reduce-scatter, shard update, all groups exchange
+                                   their shard, node all-gather; numerically the same (DESIGN §7) */
+       DASO_MODE_FUSED = 2 };   /* v3: the sharded batch with the node tier (gradient reduce over
+                                   peers + update/merge/pack + parameter all-gather) in ONE kernel
+                                   over NVLink peer memory (CUDA IPC); G <= 8; caller buffers must
+                                   be cudaMalloc-backed (torch's default allocator is) */
 
 const char* daso_status_string(daso_status s);
 const char* daso_version(void);
@@ -133,8 +137,10 @@ size_t daso_padded_numel(size_t n, int gpus_per_node);
 
 /* Attach the caller's flat fp32 buckets ("buffer packaging"): params x[n],
  * grads g[n], momentum v[n], device pointers on the ctx's device, 16-byte aligned.
- * DASO_MODE_SHARDED: each buffer must hold daso_padded_numel(n, G) elements with a
- * zero pad (x, g, v); the faithful mode touches only the first n.
+ * DASO_MODE_SHARDED / DASO_MODE_FUSED: each buffer must hold daso_padded_numel(n, G)
+ * elements with a zero pad (x, g, v); the faithful mode touches only the first n.
+ * DASO_MODE_FUSED: collective over the node — exchanges CUDA IPC handles of x and g
+ * with the node peers, which then read g and write x of this rank directly.
  * Caller-owned; they must stay alive and unmoved until daso_finalize.  x must be
  * identical on every rank (R17) and v zero-initialised by the caller.  The library
  * allocates its ring of exchange slots here: [P][n_pad] wire elements (n_pad = n

@@ -13,6 +13,7 @@
 // Data layout in HBM: caller-owned flat fp32 x, g, v [n_pad];
 // library-owned ring slot [P][seg] wire elements (seg = n_pad in the faithful mode,
 // n_pad / G in the sharded mode); 4-byte non-finite flag.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -45,6 +46,14 @@ struct daso_ctx {
 
     bool inflight = false;
     int infl_group = -1, infl_S = 0;
+
+    // fused mode: node peers' buffers mapped through CUDA IPC (NVLink peer memory)
+    float* peer_x[daso::kMaxPeers] = {};
+    float* peer_g[daso::kMaxPeers] = {};
+    unsigned long long* peer_sig[daso::kMaxPeers] = {};
+    unsigned long long* sig = nullptr;   // own [2][G] signals followed by the CTA counter
+    unsigned long long epoch = 0;
+    std::vector<void*> ipc_opened;
 
     daso_record last{};
     std::string err;
@@ -315,6 +324,142 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
     return DASO_OK;
 }
 
+// ---- fused (v3) batch: the sharded batch with the node tier inside one kernel ----------
+daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s) {
+    if (c->G == 1) return step_sharded(c, r, lr, s);   // no node tier
+    const bool global = c->P > 1;
+    const int64_t sh = c->seg;
+    const int64_t off = int64_t(c->local) * sh;
+    const bool merge = global && r.merge;
+    const bool send = global && r.send;
+    daso::PeerArgs pa;
+    pa.a = base_args(c, off, sh, lr);
+    int ops = daso::OP_UPDATE;
+    if (merge) {
+        STATUS_TRY(wait_exchange(c, s));
+        ops |= daso::OP_MERGE;
+        pa.a.den = float(2 * r.merge_S + c->P);
+        c->inflight = false;
+    }
+    if (send) {
+        ops |= daso::OP_PACK;
+        pa.a.pack_out = own_segment(c);
+    }
+    for (int q = 0; q < c->G; ++q) {
+        pa.xp[q] = c->peer_x[q] + off;
+        pa.gp[q] = c->peer_g[q] + off;
+        pa.sig_peer[q] = c->peer_sig[q];
+    }
+    pa.sig_me = c->sig;
+    pa.done = reinterpret_cast<unsigned*>(c->sig + 2 * c->G);
+    pa.err = c->d_flag;
+    pa.epoch = ++c->epoch;
+    pa.G = c->G;
+    pa.me = c->local;
+    {
+        // HBM bytes on THIS GPU per shard element: own x r + w, v r + w, own g r
+        // (20) + the G-1 peers reading this GPU's g and writing its x (8 (G-1)) + slot rows / pack.
+        // NVLink per direction: (G-1) * 4 B per shard element (bench.py reports it separately).
+        const double wb = double(c->wire_bytes);
+        double per = 20.0 + 8.0 * (c->G - 1) + ((ops & daso::OP_MERGE) ? c->P * wb : 0) +
+                     ((ops & daso::OP_PACK) ? wb : 0);
+        Span sp(c, s, PH_KERNEL, per * double(sh));
+        KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
+    }
+    if (send) {
+        STATUS_TRY(start_exchange(c, s));
+        if (r.blocking) {
+            STATUS_TRY(wait_exchange(c, s));
+            // blocking average on the shard, then re-publish it to the node peers
+            daso::KernelArgs av = base_args(c, off, sh, 0.f);
+            av.den = float(c->P);
+            KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+            for (int q = 0; q < c->G; ++q) {
+                if (q == c->local) continue;
+                CUDA_TRY(c, cudaMemcpyAsync(c->peer_x[q] + off, c->x + off, size_t(sh) * 4, cudaMemcpyDeviceToDevice, s));
+            }
+            // the peers must see every shard before their next read of x: node barrier
+            NCCL_TRY(c, ncclAllReduce(c->sig + 2 * c->G + 1, c->sig + 2 * c->G + 1, 1, ncclUint64, ncclSum,
+                                      c->node_comm, s));
+        } else {
+            c->inflight = true;
+            c->infl_group = int(r.send_group);
+            c->infl_S = int(r.S);
+        }
+    }
+    return DASO_OK;
+}
+
+typedef CUresult (*PfnAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+PfnAddressRange address_range_fn() {
+    static PfnAddressRange fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PfnAddressRange>(p);
+    }
+    return fn;
+}
+
+// Exchange CUDA IPC handles of x, g and the signal array over the node communicator and
+// map every node peer's buffers into this process (peer access over NVLink).
+struct IpcExport {
+    cudaIpcMemHandle_t h[3];
+    uint64_t base[3];
+    uint64_t off[3];
+};
+
+daso_status setup_peers(daso_ctx* c) {
+    PfnAddressRange range = address_range_fn();
+    if (!range) return c->fail(DASO_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    const size_t sig_bytes = (2 * size_t(c->G) + 2) * sizeof(unsigned long long);
+    CUDA_TRY(c, cudaMalloc(&c->sig, sig_bytes));
+    CUDA_TRY(c, cudaMemset(c->sig, 0, sig_bytes));
+    void* bufs[3] = {c->x, c->g, c->sig};
+    IpcExport mine{};
+    for (int b = 0; b < 3; ++b) {
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, CUdeviceptr(bufs[b])) != CUDA_SUCCESS)
+            return c->fail(DASO_ERR_ARGUMENT, "buffer %d is not a device allocation", b);
+        CUDA_TRY(c, cudaIpcGetMemHandle(&mine.h[b], reinterpret_cast<void*>(base)));
+        mine.base[b] = uint64_t(base);
+        mine.off[b] = uint64_t(CUdeviceptr(bufs[b]) - base);
+    }
+    std::vector<IpcExport> all(c->G);
+    void* dbuf = nullptr;
+    CUDA_TRY(c, cudaMalloc(&dbuf, sizeof(IpcExport) * c->G));
+    CUDA_TRY(c, cudaMemcpy(static_cast<char*>(dbuf) + sizeof(IpcExport) * c->local, &mine, sizeof mine,
+                           cudaMemcpyHostToDevice));
+    NCCL_TRY(c, ncclAllGather(static_cast<char*>(dbuf) + sizeof(IpcExport) * c->local, dbuf, sizeof(IpcExport),
+                              ncclUint8, c->node_comm, c->side));
+    CUDA_TRY(c, cudaStreamSynchronize(c->side));
+    CUDA_TRY(c, cudaMemcpy(all.data(), dbuf, sizeof(IpcExport) * c->G, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    for (int q = 0; q < c->G; ++q) {
+        void* mapped[3] = {nullptr, nullptr, nullptr};
+        if (q == c->local) {
+            for (int b = 0; b < 3; ++b) mapped[b] = reinterpret_cast<char*>(bufs[b]) - all[q].off[b];
+        } else {
+            for (int b = 0; b < 3; ++b) {
+                for (int e = 0; e < b; ++e)   // one mapping per distinct allocation of the peer
+                    if (all[q].base[e] == all[q].base[b]) mapped[b] = mapped[e];
+                if (!mapped[b]) {
+                    CUDA_TRY(c, cudaIpcOpenMemHandle(&mapped[b], all[q].h[b], cudaIpcMemLazyEnablePeerAccess));
+                    c->ipc_opened.push_back(mapped[b]);
+                }
+            }
+        }
+        c->peer_x[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[0]) + all[q].off[0]);
+        c->peer_g[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[1]) + all[q].off[1]);
+        c->peer_sig[q] = reinterpret_cast<unsigned long long*>(static_cast<char*>(mapped[2]) + all[q].off[2]);
+    }
+    return DASO_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -356,7 +501,9 @@ daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S
     if (world < 1 || gpus_per_node < 1 || world % gpus_per_node != 0 || B < 1) return DASO_ERR_CONFIG;
     if (cfg->rank < 0 || cfg->rank >= world) return DASO_ERR_RANGE;
     if (cfg->wire != DASO_WIRE_BF16 && cfg->wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
-    if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED) return DASO_ERR_ARGUMENT;
+    if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED && cfg->mode != DASO_MODE_FUSED)
+        return DASO_ERR_ARGUMENT;
+    if (cfg->mode == DASO_MODE_FUSED && gpus_per_node > daso::kMaxPeers) return DASO_ERR_CONFIG;
     daso_sched_config sc{};
     sc.B_init = B;
     sc.S_init = S;
@@ -420,12 +567,13 @@ daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n) {
     c->v = v;
     c->n = int64_t(n);
     c->n_pad = (int64_t(n) + q - 1) / q * q;
-    c->seg = c->cfg.mode == DASO_MODE_SHARDED ? c->n_pad / c->G : c->n_pad;
+    c->seg = c->cfg.mode == DASO_MODE_FAITHFUL ? c->n_pad : c->n_pad / c->G;
     if (c->P > 1) {
         const size_t bytes = size_t(c->P) * size_t(c->seg) * c->wire_bytes;
         CUDA_TRY(c, cudaMalloc(&c->slot, bytes));
         CUDA_TRY(c, cudaMemset(c->slot, 0, bytes));
     }
+    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1) STATUS_TRY(setup_peers(c));
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->bound = true;
     return DASO_OK;
@@ -512,6 +660,7 @@ daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_rec
     if (r.merge && c->P > 1 && !c->inflight)
         return c->fail(DASO_ERR_PROTOCOL, "schedule merge at step %lld but nothing in flight", (long long)r.step);
     if (c->cfg.mode == DASO_MODE_SHARDED) return step_sharded(c, r, lr, s);
+    if (c->cfg.mode == DASO_MODE_FUSED) return step_fused(c, r, lr, s);
     return step_faithful(c, r, lr, s);
 }
 
@@ -571,6 +720,7 @@ daso_status daso_check_finite(daso_ctx* c, void* stream) {
     CUDA_TRY(c, cudaMemcpyAsync(&h, c->d_flag, sizeof h, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(uint32_t), s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (h & 2u) return c->fail(DASO_ERR_PROTOCOL, "node barrier timed out in the fused kernel (a peer never arrived)");
     if (h) return c->fail(DASO_ERR_NONFINITE, "non-finite parameter written");
     return DASO_OK;
 }
@@ -589,6 +739,15 @@ daso_status daso_finalize(daso_ctx* c) {
     daso_status st = DASO_OK;
     if (c->side) cudaStreamSynchronize(c->side);   // drain an in-flight exchange
     cudaDeviceSynchronize();
+    if (!c->ipc_opened.empty() || c->sig) {
+        // no node peer may still touch this rank's memory: node barrier before unmapping
+        if (c->node_comm && c->sig && c->side) {
+            ncclAllReduce(c->sig + 2 * c->G + 1, c->sig + 2 * c->G + 1, 1, ncclUint64, ncclSum, c->node_comm, c->side);
+            cudaStreamSynchronize(c->side);
+        }
+        for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+        if (c->sig) cudaFree(c->sig);
+    }
     ncclComm_t comms[3] = {c->group_comm, c->node_comm, c->world_comm};
     for (ncclComm_t m : comms) {
         if (!m) continue;

@@ -50,6 +50,21 @@ struct KernelArgs {
 };
 
 int launch_fused(int ops, int wire, const KernelArgs& a, void* stream);
+
+// fused node-local tier over NVLink peer memory (peer.cu)
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+    KernelArgs a;                              // x, v, pack_out, slot: this rank's shard
+    float* xp[kMaxPeers] = {};                 // every node peer's x at this shard (xp[me] = own)
+    const float* gp[kMaxPeers] = {};           // every node peer's g at this shard
+    unsigned long long* sig_peer[kMaxPeers] = {};   // every peer's signal array [2][G]
+    unsigned long long* sig_me = nullptr;      // this rank's signal array
+    unsigned* done = nullptr;                  // this rank's CTA completion counter
+    uint32_t* err = nullptr;                   // bit 1 set on a barrier timeout
+    unsigned long long epoch = 0;              // monotonically increasing barrier value
+    int G = 1, me = 0;
+};
+int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream);
 int set_kernel_impl(int impl);   // returns the previous selection
 int launch_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count,
                   float* dst, void* stream);

@@ -15,7 +15,7 @@ from . import _lib as L
 from ._lib import DasoError, Record, check, lib  # noqa: F401
 
 WIRES = {"bf16": L.WIRE_BF16, "fp32": L.WIRE_FP32}
-MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED}
+MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED}
 
 
 def _torch():
@@ -104,7 +104,7 @@ class Ctx:
         for t, nm in ((x, "x"), (g, "g"), (v, "v")):
             _dev_f32(t, nm)
         n = x.numel() if n is None else int(n)
-        need = daso_padded_numel(n, self.G) if self.mode == "sharded" else n
+        need = daso_padded_numel(n, self.G) if self.mode != "faithful" else n
         if min(x.numel(), g.numel(), v.numel()) < need:
             raise ValueError(f"buckets must hold {need} elements in {self.mode} mode")
         self._keep = (x, g, v)

@@ -99,7 +99,7 @@ def check(ranks, P, G, B, S, steps=20, d=1000, b=32, lr=0.01, mu=0.9, wd=1e-4, w
 TOY = ["--B", "4", "--S", "1"]
 
 
-@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused"])
 def test_world1_is_plain_sgd(tmp_path, mode):
     ranks = run_world(str(tmp_path), 1, TOY + ["--P", "1", "--G", "1", "--mode", mode, "--wire", "fp32"])
     check(ranks, 1, 1, 4, 1, wire="fp32")
@@ -107,8 +107,9 @@ def test_world1_is_plain_sgd(tmp_path, mode):
 
 @pytest.mark.parametrize("P,G", [(2, 1), (1, 2)])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
-def test_world2_toy(tmp_path, P, G, wire):
-    ranks = run_world(str(tmp_path), 2, TOY + ["--P", str(P), "--G", str(G), "--wire", wire])
+@pytest.mark.parametrize("mode", ["faithful", "fused"])
+def test_world2_toy(tmp_path, P, G, wire, mode):
+    ranks = run_world(str(tmp_path), 2, TOY + ["--P", str(P), "--G", str(G), "--wire", wire, "--mode", mode])
     check(ranks, P, G, 4, 1, wire=wire)
 
 
@@ -124,14 +125,17 @@ def test_world2_S_equals_B(tmp_path):
     check(ranks, 2, 1, 2, 2, wire="fp32")
 
 
-def test_world2_blocking_fp32_is_flat_sync(tmp_path):
+@pytest.mark.parametrize("P,G,mode", [(2, 1, "faithful"), (2, 2, "faithful"), (2, 2, "sharded"), (2, 2, "fused")])
+def test_blocking_fp32_is_flat_sync(tmp_path, P, G, mode):
     """B=1, S=0, fp32 wire: DASO == synchronous SGD over the concatenated batch."""
-    ranks = run_world(str(tmp_path), 2, ["--P", "2", "--G", "1", "--B", "1", "--S", "0", "--wire", "fp32"])
-    check(ranks, 2, 1, 1, 0, wire="fp32")
-    np.testing.assert_array_equal(ranks[0]["cks"], ranks[1]["cks"])   # blocking: all ranks identical
+    ranks = run_world(str(tmp_path), P * G, ["--P", str(P), "--G", str(G), "--B", "1", "--S", "0", "--wire", "fp32",
+                                             "--mode", mode])
+    check(ranks, P, G, 1, 0, wire="fp32")
+    for r in ranks[1:]:
+        np.testing.assert_array_equal(r["cks"], ranks[0]["cks"])   # blocking: all ranks identical
 
 
-@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused"])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
 def test_world4_toy_config1(tmp_path, mode, wire):
     """Config 1 proper: 2 virtual nodes x 2 GPUs, B=4, S=1, 20 steps."""
@@ -147,12 +151,13 @@ def test_world4_split_api_equals_step(tmp_path):
 
 
 @pytest.mark.parametrize("P,G", [(4, 1), (1, 4)])
-def test_world4_other_topologies(tmp_path, P, G):
-    ranks = run_world(str(tmp_path), 4, TOY + ["--P", str(P), "--G", str(G)])
+@pytest.mark.parametrize("mode", ["faithful", "fused"])
+def test_world4_other_topologies(tmp_path, P, G, mode):
+    ranks = run_world(str(tmp_path), 4, TOY + ["--P", str(P), "--G", str(G), "--mode", mode])
     check(ranks, P, G, 4, 1)
 
 
-@pytest.mark.parametrize("mode", ["faithful", "sharded"])
+@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused"])
 def test_world4_full_schedule(tmp_path, mode):
     args = ["--P", "2", "--G", "2", "--B", "4", "--S", "1", "--warmup", "1", "--cooldown", "1", "--epochs", "5",
             "--spe", "8", "--steps", "40", "--flags", "01100", "--mode", mode]
