@@ -102,6 +102,25 @@ daso_status daso_sched_create(const daso_sched_config* cfg, daso_sched** out);
 daso_status daso_sched_next(daso_sched* s, int plateau, daso_record* out);
 daso_status daso_sched_destroy(daso_sched* s);
 
+/* ------------------------------------------------- plateau detector and LR
+ * Host-only.  P:162 "When the training loss plateaus, i.e. the training loss is not
+ * decreasing by more than a set percentage threshold, the scheduler decreases the
+ * learning rate by a set factor"; "decays by a factor of 0.5 when the training
+ * cross entropy loss is stable for 5 epochs"; P:99 the same events halve B and S.
+ * Reading R20: feed one mean training loss per epoch; an epoch improves iff
+ * loss < best - threshold * |best|; `patience` consecutive non-improving epochs set
+ * *fired = 1 (then the count restarts).  Pass the result as `plateau` at the next
+ * epoch's first daso_step.  Errors: DASO_ERR_CONFIG (patience < 1, threshold < 0),
+ * DASO_ERR_NONFINITE (NaN/Inf loss: training diverged). */
+typedef struct daso_plateau daso_plateau;
+daso_status daso_plateau_create(int patience, double threshold, daso_plateau** out);
+daso_status daso_plateau_update(daso_plateau* p, double loss, int* fired);
+daso_status daso_plateau_destroy(daso_plateau* p);
+/* Learning rate at global batch `step`: linear warm-up from 0 to peak = base_lr * world
+ * over warmup_epochs, then peak * factor^n_plateaus. */
+daso_status daso_lr_at(int64_t step, int steps_per_epoch, double base_lr, int world, int warmup_epochs,
+                       double factor, int n_plateaus, double* out);
+
 /* ------------------------------------------------------------ full context */
 typedef struct daso_ctx daso_ctx;
 

@@ -73,6 +73,11 @@ _SIG = {
     "daso_sched_next": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Record)]),
     "daso_sched_destroy": (C.c_int, [C.c_void_p]),
     "daso_get_unique_id": (C.c_int, [C.c_void_p]),
+    "daso_plateau_create": (C.c_int, [C.c_int, C.c_double, C.POINTER(C.c_void_p)]),
+    "daso_plateau_update": (C.c_int, [C.c_void_p, C.c_double, C.POINTER(C.c_int)]),
+    "daso_plateau_destroy": (C.c_int, [C.c_void_p]),
+    "daso_lr_at": (C.c_int, [C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int,
+                             C.POINTER(C.c_double)]),
     "daso_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Config),
                             C.c_void_p]),
     "daso_bind": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),

@@ -2,6 +2,9 @@
 // halving / reset rule (§3), with the readings R6, R8-R10, R13-R15
 // of DESIGN.md §3.  Bit-exact contract with the independent CPU oracle
 // (oracle/schedule.py), checked record by record in tests/test_schedule_abi.py.
+#include <cmath>
+#include <new>
+
 #include "daso_internal.h"
 
 namespace daso {
@@ -108,9 +111,66 @@ daso_record Schedule::next(int plateau) {
     return r;
 }
 
+// Loss-plateau detector ("not decreasing by more than a set percentage threshold",
+// P:172 "stable for 5 epochs"; reading R20): an epoch improves iff
+// loss < best - threshold * |best|; `patience` consecutive non-improving epochs fire.
+struct Plateau {
+    int patience;
+    double threshold;
+    double best = INFINITY;
+    int stable = 0;
+    int update(double loss) {
+        if (std::isinf(best) || loss < best - threshold * std::fabs(best)) {
+            best = loss;
+            stable = 0;
+            return 0;
+        }
+        if (++stable >= patience) {
+            stable = 0;
+            return 1;
+        }
+        return 0;
+    }
+};
+
 }  // namespace daso
 
 extern "C" {
+
+daso_status daso_plateau_create(int patience, double threshold, daso_plateau** out) {
+    if (!out) return DASO_ERR_ARGUMENT;
+    if (patience < 1 || !(threshold >= 0)) return DASO_ERR_CONFIG;
+    auto* p = new (std::nothrow) daso::Plateau{patience, threshold};
+    if (!p) return DASO_ERR_ARGUMENT;
+    *out = reinterpret_cast<daso_plateau*>(p);
+    return DASO_OK;
+}
+
+daso_status daso_plateau_update(daso_plateau* h, double loss, int* fired) {
+    if (!h || !fired) return DASO_ERR_ARGUMENT;
+    if (!std::isfinite(loss)) return DASO_ERR_NONFINITE;
+    *fired = reinterpret_cast<daso::Plateau*>(h)->update(loss);
+    return DASO_OK;
+}
+
+daso_status daso_plateau_destroy(daso_plateau* h) {
+    delete reinterpret_cast<daso::Plateau*>(h);
+    return DASO_OK;
+}
+
+daso_status daso_lr_at(int64_t step, int steps_per_epoch, double base_lr, int world, int warmup_epochs,
+                       double factor, int n_plateaus, double* out) {
+    if (!out) return DASO_ERR_ARGUMENT;
+    if (steps_per_epoch < 1 || world < 1 || warmup_epochs < 0 || step < 0 || n_plateaus < 0) return DASO_ERR_CONFIG;
+    const double peak = base_lr * world;                       // P:172 "scaled with the number of global processes"
+    const int64_t warm = int64_t(warmup_epochs) * steps_per_epoch;
+    if (step < warm) {
+        *out = peak * double(step + 1) / double(warm);          // P:212 "increased from 0.0 to" the peak
+    } else {
+        *out = peak * std::pow(factor, double(n_plateaus));    // P:162 "decreases the learning rate by a set factor"
+    }
+    return DASO_OK;
+}
 
 daso_status daso_sched_create(const daso_sched_config* cfg, daso_sched** out) {
     if (!cfg || !out) return DASO_ERR_ARGUMENT;

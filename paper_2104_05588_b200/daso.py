@@ -69,6 +69,35 @@ class Schedule:
     __del__ = close
 
 
+class PlateauDetector:
+    """daso_plateau_*: one mean training loss per epoch -> plateau flag."""
+
+    def __init__(self, patience: int = 5, threshold: float = 0.01):
+        h = C.c_void_p()
+        check(lib().daso_plateau_create(int(patience), float(threshold), C.byref(h)), "daso_plateau_create")
+        self._h = h
+
+    def update(self, loss: float) -> int:
+        f = C.c_int(0)
+        check(lib().daso_plateau_update(self._h, float(loss), C.byref(f)), "daso_plateau_update")
+        return int(f.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().daso_plateau_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def daso_lr_at(step: int, steps_per_epoch: int, base_lr: float, world: int, warmup_epochs: int, factor: float,
+               n_plateaus: int) -> float:
+    out = C.c_double()
+    check(lib().daso_lr_at(int(step), int(steps_per_epoch), float(base_lr), int(world), int(warmup_epochs),
+                           float(factor), int(n_plateaus), C.byref(out)), "daso_lr_at")
+    return float(out.value)
+
+
 # ------------------------------------------------------------------ context
 def daso_get_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
@@ -250,10 +279,17 @@ def daso_flat_layout(numels: Iterable[int], align: int = 64) -> tuple[list[int],
     return [int(offs[i]) for i in range(n)], int(tot.value)
 
 
+def _dense_f32(t, name: str):
+    torch = _torch()
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_non_overlapping_and_dense()):
+        raise ValueError(f"{name} must be a dense (any memory format) float32 CUDA tensor")
+
+
 def daso_k_gather(tensors, dst, offsets, stream=None):
+    """Copy each tensor's memory block (numel floats in memory order) into dst[offset:]."""
     n = len(tensors)
     for t in tensors:
-        _dev_f32(t, "tensor")
+        _dense_f32(t, "tensor")
     src = (C.c_void_p * n)(*[t.data_ptr() for t in tensors])
     numel = (C.c_size_t * n)(*[t.numel() for t in tensors])
     offs = (C.c_size_t * n)(*offsets)
@@ -296,8 +332,10 @@ class FlatParams:
         self.x = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
         self.g = torch.zeros_like(self.x)
         self.v = torch.zeros_like(self.x)
-        daso_k_gather([p.detach().contiguous() for p in self.params], self.x, self.offsets)
+        daso_k_gather([p.detach() for p in self.params], self.x, self.offsets)
         torch.cuda.current_stream().synchronize()
+        # views keep each parameter's memory format (e.g. channels_last): the bucket holds
+        # every tensor's memory block in memory order
         for p, o in zip(self.params, self.offsets):
-            p.data = self.x[o:o + p.numel()].view_as(p)
-            p.grad = self.g[o:o + p.numel()].view_as(p)
+            p.data = self.x.as_strided(p.shape, p.stride(), o)
+            p.grad = self.g.as_strided(p.shape, p.stride(), o)
