@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--compute-ms", type=float, default=0.0,
+                    help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
+                         "the global exchange the next batch's compute hides")
     return ap.parse_args()
 
 
@@ -126,6 +129,31 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_compute(ms: float, dev):
+    """A stand-in for the next batch's forward/backward: bf16 8192^3 GEMMs totalling ~ms."""
+    if ms <= 0:
+        return lambda: None
+    import torch
+    a = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    b = torch.randn_like(a)
+    c = torch.empty_like(a)
+    for _ in range(3):
+        torch.matmul(a, b, out=c)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        torch.matmul(a, b, out=c)
+    e1.record()
+    torch.cuda.synchronize()
+    reps = max(1, round(ms / (e0.elapsed_time(e1) / 10)))
+
+    def run():
+        for _ in range(reps):
+            torch.matmul(a, b, out=c)
+    return run
 
 
 def dist_setup():
@@ -214,8 +242,10 @@ def run_ours(a):
     ctx.bind(x, g, v, n)
     stream = torch.cuda.current_stream()
 
+    compute = make_compute(a.compute_ms, dev)
     for _ in range(a.warmup):
         g.copy_(g_src)
+        compute()
         ctx.step(a.lr)
     torch.cuda.synchronize()
     ctx.trace_read(reset=True)
@@ -228,6 +258,7 @@ def run_ours(a):
     with ClockSampler(local) as clk:
         for k in range(a.steps):
             g.copy_(g_src)
+            compute()
             ev0[k].record(stream)
             r = ctx.step(a.lr)
             ev1[k].record(stream)
@@ -251,8 +282,9 @@ def run_ours(a):
                 "bytes_per_launch": tr["kernel_bytes"] / max(tr["kernel_launches"], 1),
                 "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1), "peak_source": peak_src}
     if a.mode == "fused" and G > 1:
-        # the fused node-tier kernel is NVLink-bound: (G-1)/G * 4n bytes leave and enter each GPU
-        nvl_bytes = (G - 1) * 4.0 * daso.daso_padded_numel(n, G) / G
+        # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
+        # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)
+        nvl_bytes = 2.0 * (G - 1) * 4.0 * daso.daso_padded_numel(n, G) / G
         nvl_gbs = nvl_bytes / (tr["kernel_ms"] / max(tr["kernel_launches"], 1) * 1e-3) / 1e9
         nvl_gbs = -max_over_ranks(-nvl_gbs, world)
         roofline = {"bound": "nvlink", "achieved": nvl_gbs, "peak": 770.0, "unit": "GB/s",
@@ -303,7 +335,8 @@ def run_ours(a):
                        "wire": a.wire, "parallelism": f"daso {P} virtual nodes x {G} GPUs",
                        "l2": "inputs (x, v, g = 307 MB) exceed the 126 MB L2; the untimed gradient refresh "
                              "between steps (204 MB) also flushes it",
-                       "value_def": "4 B x n params x N GPUs / ms_per_step", "step_kinds": kinds},
+                       "value_def": "4 B x n params x N GPUs / ms_per_step", "step_kinds": kinds,
+                       "compute_ms_between_steps": a.compute_ms},
             "roofline": roofline, "phases": phases, "gpu_launches": tr["kernel_launches"],
             "clocks": clk.summary(), "e2e": e2e, "finite": finite}
     if world == 1 and not a.no_cpu:

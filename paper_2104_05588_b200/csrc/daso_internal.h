@@ -66,6 +66,7 @@ struct PeerArgs {
 };
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream);
 int set_kernel_impl(int impl);   // returns the previous selection
+int current_kernel_impl();       // 0 register path, 1 TMA-staged path
 int launch_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count,
                   float* dst, void* stream);
 int launch_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets,

@@ -19,6 +19,8 @@
 // exchange kernels to run concurrently.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "daso_internal.h"
 #include "device_common.cuh"
 
@@ -27,7 +29,7 @@ namespace {
 using namespace dev;
 
 constexpr int kPeerThreads = 256;
-constexpr int kPV = 4;   // parameters per thread per iteration (one 128-bit access per stream)
+constexpr int kPV = 8;   // parameters per thread per iteration (two 128-bit accesses per stream)
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -61,25 +63,22 @@ __device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned l
     }
 }
 
-template <int OPS, int WIRE, int N>
+template <int OPS, int WIRE, int G, int N>
 __device__ __forceinline__ void peer_body(const PeerArgs& pa, int64_t i, bool& bad) {
     const KernelArgs& a = pa.a;
-    const int G = pa.G;
     float x[N], v[N], g[N];
+    float gq[G][N];
+#pragma unroll
+    for (int q = 0; q < G; ++q) ld_f32<N>(pa.gp[q] + i, gq[q]);   // all peer loads in flight first
     ld_f32<N>(a.x + i, x);
     ld_f32<N>(a.v + i, v);
-    float gq[kMaxPeers][N];
-#pragma unroll
-    for (int q = 0; q < kMaxPeers; ++q)
-        if (q < G) ld_f32<N>(pa.gp[q] + i, gq[q]);
 #pragma unroll
     for (int j = 0; j < N; ++j) g[j] = gq[0][j];
 #pragma unroll
-    for (int q = 1; q < kMaxPeers; ++q)
-        if (q < G) {
+    for (int q = 1; q < G; ++q) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) g[j] += gq[q][j];
-        }
+        for (int j = 0; j < N; ++j) g[j] += gq[q][j];                // ascending local id (R18)
+    }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
@@ -102,16 +101,14 @@ __device__ __forceinline__ void peer_body(const PeerArgs& pa, int64_t i, bool& b
         for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;
     }
 #pragma unroll
-    for (int q = 0; q < kMaxPeers; ++q)
-        if (q < G) st_f32<N>(pa.xp[q] + i, x);
+    for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[q] + i, x);
 #pragma unroll
     for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
     if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
 }
 
-template <int OPS, int WIRE>
+template <int OPS, int WIRE, int G>
 __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
-    const int G = pa.G;
     // 1. start barrier
     if (blockIdx.x == 0 && threadIdx.x < G) {
         __threadfence_system();
@@ -126,10 +123,10 @@ __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
     const int64_t nch = n / kPV;
     const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
     for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
-        peer_body<OPS, WIRE, kPV>(pa, c * kPV, bad);
+        peer_body<OPS, WIRE, G, kPV>(pa, c * kPV, bad);
     if (blockIdx.x == gridDim.x - 1) {
         const int64_t i = nch * kPV + threadIdx.x;
-        if (i < n) peer_body<OPS, WIRE, 1>(pa, i, bad);
+        if (i < n) peer_body<OPS, WIRE, G, 1>(pa, i, bad);
     }
     if (pa.a.flag != nullptr) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
@@ -149,22 +146,219 @@ __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
     }
 }
 
-template <int OPS, int WIRE>
+int peer_blocks_per_sm() {   // grid = SMs x this (DASO_PEER_BPSM, default 2 (measured best)); one-shot if larger
+    static int v = 0;
+    if (v == 0) {
+        const char* e = getenv("DASO_PEER_BPSM");
+        v = e ? atoi(e) : 2;
+        if (v < 1) v = 1;
+    }
+    return v;
+}
+
+template <int OPS, int WIRE, int G>
 int launch_peer_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     const int64_t nch = pa.a.n / kPV;
     int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * 2));
-    peer_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
+    peer_kernel<OPS, WIRE, G><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
     return int(cudaGetLastError());
+}
+
+
+// ---- TMA-staged variant (daso_kernel_impl(1)): the same batch with the peer gradient
+// loads and the peer parameter stores done by the bulk-copy engine (cp.async.bulk on
+// NVLink-mapped global addresses) through an mbarrier ring of shared-memory stages, one
+// persistent CTA per SM.  Per tile: own x, v + G gradient tiles (G-1 remote) in; x out
+// to G peers (G-1 remote), v and the packed row out locally.
+constexpr int kPT = 2048;
+
+struct PeerTmaLayout {
+    uint32_t x, v, g, slot, pack, bytes;
+};
+__host__ __device__ inline PeerTmaLayout peer_tma_layout(int ops, int G, int P, int wb) {
+    PeerTmaLayout L{};
+    uint32_t o = 0;
+    L.x = o; o += kPT * 4;
+    L.v = o; o += kPT * 4;
+    L.g = o; o += uint32_t(G) * kPT * 4;
+    L.slot = o; if (ops & OP_MERGE) o += uint32_t(P) * kPT * wb;
+    L.pack = o; if (ops & OP_PACK) o += kPT * wb;
+    L.bytes = (o + 127) / 128 * 128;
+    return L;
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <int OPS, int WIRE, int G>
+__global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArgs pa, int NS) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const KernelArgs& a = pa.a;
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, a.P, wb);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * L.bytes);
+    const bool leader = threadIdx.x == 0;
+    // 1. start barrier
+    if (blockIdx.x == 0 && threadIdx.x < G) {
+        __threadfence_system();
+        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
+    }
+    if (leader) {
+        for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + q, pa.epoch, pa.err);
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_global();
+    }
+    __syncthreads();
+
+    const int64_t ntiles = a.n / kPT;
+    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue_load = [&](int64_t k) {
+        const int s = int(k % NS);
+        unsigned char* st = smem + size_t(s) * L.bytes;
+        const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kPT;
+        uint32_t tx = (2u + G) * kPT * 4u;
+        if constexpr ((OPS & OP_MERGE) != 0) tx += uint32_t(a.P) * kPT * wb;
+        mbar_expect_tx(&full[s], tx);
+        bulk_g2s(st + L.x, a.x + e0, kPT * 4, &full[s]);
+        bulk_g2s(st + L.v, a.v + e0, kPT * 4, &full[s]);
+#pragma unroll
+        for (int q = 0; q < G; ++q) bulk_g2s(st + L.g + uint32_t(q) * kPT * 4, pa.gp[q] + e0, kPT * 4, &full[s]);
+        if constexpr ((OPS & OP_MERGE) != 0) {
+            for (int p = 0; p < a.P; ++p)
+                bulk_g2s(st + L.slot + uint32_t(p) * kPT * wb,
+                         static_cast<const unsigned char*>(a.slot) + (p * a.slot_stride + e0) * wb, kPT * wb, &full[s]);
+        }
+    };
+    if (leader)
+        for (int64_t k = 0; k < my && k < NS; ++k) issue_load(k);
+
+    bool bad = false;
+    for (int64_t k = 0; k < my; ++k) {
+        const int s = int(k % NS);
+        unsigned char* st = smem + size_t(s) * L.bytes;
+        mbar_wait(&full[s], uint32_t((k / NS) & 1));
+        const int i = threadIdx.x * 8;
+        float x[8], v[8], g[8];
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.v, i, v);
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g, i, g);
+#pragma unroll
+        for (int q = 1; q < G; ++q) {
+            float t[8];
+            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g + uint32_t(q) * kPT * 4, i, t);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g[j] += t[j];                        // ascending local id (R18)
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
+            v[j] = fmaf(a.mu, v[j], d);
+            x[j] = fmaf(-a.lr, v[j], x[j]);
+        }
+        if constexpr ((OPS & OP_MERGE) != 0) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int p = 0; p < a.P; ++p) {
+                float sv[8];
+                Wire<WIRE>::template load_smem<8>(st + L.slot + uint32_t(p) * kPT * wb, i, sv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += sv[j] - x[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
+        }
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(st + L.x, i, x);
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(st + L.v, i, v);
+        if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(st + L.pack, i, x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
+        fence_async_smem();
+        __syncthreads();
+        if (leader) {
+            const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kPT;
+            bulk_s2g(a.v + e0, st + L.v, kPT * 4);
+#pragma unroll
+            for (int q = 0; q < G; ++q) bulk_s2g(pa.xp[q] + e0, st + L.x, kPT * 4);
+            if constexpr ((OPS & OP_PACK) != 0)
+                bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, st + L.pack, kPT * wb);
+            bulk_commit();
+            if (k >= 1 && k - 1 + NS < my) {
+                bulk_wait_read<1>();
+                issue_load(k - 1 + NS);
+            }
+        }
+    }
+    if (leader) bulk_wait_all();
+    if (blockIdx.x == gridDim.x - 1)
+        for (int64_t e = ntiles * kPT + threadIdx.x; e < a.n; e += blockDim.x) peer_body<OPS, WIRE, G, 1>(pa, e, bad);
+    if (a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
+    }
+    // 3. end barrier (all bulk stores of this CTA are complete: wait_group 0 above)
+    __syncthreads();
+    if (leader) {
+        fence_proxy_async_global();
+        __threadfence_system();
+        const unsigned prev = atomicAdd(pa.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
+            __threadfence_system();
+            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
+            for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + G + q, pa.epoch, pa.err);
+        }
+    }
+}
+
+template <int OPS, int WIRE, int G>
+int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, pa.a.P, wb);
+    const int budget = 200 * 1024;
+    const int NS = int(std::min<int64_t>(8, (budget - 64) / L.bytes));
+    if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    const size_t smem = size_t(NS) * L.bytes + 8 * size_t(NS);
+    peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(sms)), dim3(kPeerThreads), smem, s>>>(pa, NS);
+    return int(cudaGetLastError());
+}
+
+template <int OPS, int WIRE, int G>
+int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
+    const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
+                      reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
+    if (current_kernel_impl() == 1 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
+    return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
+}
+
+template <int OPS, int WIRE>
+int dispatch_g(const PeerArgs& pa, cudaStream_t s, int sms) {
+    switch (pa.G) {
+        case 1: return launch_peer_any<OPS, WIRE, 1>(pa, s, sms);
+        case 2: return launch_peer_any<OPS, WIRE, 2>(pa, s, sms);
+        case 3: return launch_peer_any<OPS, WIRE, 3>(pa, s, sms);
+        case 4: return launch_peer_any<OPS, WIRE, 4>(pa, s, sms);
+        case 5: return launch_peer_any<OPS, WIRE, 5>(pa, s, sms);
+        case 6: return launch_peer_any<OPS, WIRE, 6>(pa, s, sms);
+        case 7: return launch_peer_any<OPS, WIRE, 7>(pa, s, sms);
+        case 8: return launch_peer_any<OPS, WIRE, 8>(pa, s, sms);
+        default: return int(cudaErrorInvalidValue);
+    }
 }
 
 template <int WIRE>
 int dispatch_peer(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
     switch (ops) {
-        case OP_UPDATE: return launch_peer_t<OP_UPDATE, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_PACK: return launch_peer_t<OP_UPDATE | OP_PACK, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_MERGE: return launch_peer_t<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_MERGE | OP_PACK: return launch_peer_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
+        case OP_UPDATE: return dispatch_g<OP_UPDATE, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_PACK: return dispatch_g<OP_UPDATE | OP_PACK, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_MERGE: return dispatch_g<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_MERGE | OP_PACK: return dispatch_g<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
         default: return int(cudaErrorInvalidValue);
     }
 }

@@ -279,9 +279,20 @@ def daso_flat_layout(numels: Iterable[int], align: int = 64) -> tuple[list[int],
     return [int(offs[i]) for i in range(n)], int(tot.value)
 
 
+def _is_dense(t) -> bool:
+    """True if the tensor's elements exactly fill numel consecutive slots (any dim order)."""
+    dims = sorted((st, sz) for st, sz in zip(t.stride(), t.shape) if sz != 1)
+    expect = 1
+    for st, sz in dims:
+        if st != expect:
+            return False
+        expect *= sz
+    return True
+
+
 def _dense_f32(t, name: str):
     torch = _torch()
-    if not (t.is_cuda and t.dtype == torch.float32 and t.is_non_overlapping_and_dense()):
+    if not (t.is_cuda and t.dtype == torch.float32 and _is_dense(t)):
         raise ValueError(f"{name} must be a dense (any memory format) float32 CUDA tensor")
 
 

@@ -41,6 +41,7 @@ def parse(argv=None):
     ap.add_argument("--wire", default="bf16")
     ap.add_argument("--mode", default="faithful")
     ap.add_argument("--split", action="store_true", help="drive the split API instead of daso_step")
+    ap.add_argument("--kernel", default="", help="ldg | tma: fused-kernel data path (daso_kernel_impl)")
     ap.add_argument("--out", required=True)
     return ap.parse_args(argv)
 
@@ -50,6 +51,8 @@ def run_toy(a, rank: int = 0, world: int = 1, uid: bytes | None = None):
     import paper_2104_05588_b200 as daso
     from paper_2104_05588_b200 import Schedule
 
+    if a.kernel:
+        daso.daso_kernel_impl(a.kernel)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     dev = torch.device("cuda", torch.cuda.current_device())

@@ -163,3 +163,15 @@ def test_world4_full_schedule(tmp_path, mode):
             "--spe", "8", "--steps", "40", "--flags", "01100", "--mode", mode]
     ranks = run_world(str(tmp_path), 4, args)
     check(ranks, 2, 2, 4, 1, steps=40, warm=1, cool=1, epochs=5, spe=8, flags="01100")
+
+
+@pytest.mark.parametrize("P,G", [(2, 2), (1, 4)])
+def test_fused_tma_path_bit_identical(tmp_path, P, G):
+    """The TMA-staged fused kernel (bulk copies over NVLink) computes exactly what the
+    register-path fused kernel computes; d = 8192 spans several 2048-element tiles."""
+    args = TOY + ["--P", str(P), "--G", str(G), "--mode", "fused", "--d", "8192", "--steps", "12"]
+    a = run_world(str(tmp_path / "a"), 4, args + ["--kernel", "ldg"])
+    b = run_world(str(tmp_path / "b"), 4, args + ["--kernel", "tma"])
+    for ra, rb in zip(a, b):
+        np.testing.assert_array_equal(ra["trace"].view(np.uint32), rb["trace"].view(np.uint32))
+    check(b, P, G, 4, 1, steps=12, d=8192)
