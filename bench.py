@@ -69,6 +69,17 @@ def topology(a, world):
     return P, G
 
 
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant kernel
+    from the committed `ncu --set full` capture summary (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    d = json.load(open(p))
+    e = d.get(kernel_prefix)
+    return (e["dram_bytes_per_launch"], e.get("source")) if e else (None, None)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -281,6 +292,10 @@ def run_ours(a):
                 "kernel": "fused_kernel (K1/K2/K3: update [+merge] [+bf16 pack])",
                 "bytes_per_launch": tr["kernel_bytes"] / max(tr["kernel_launches"], 1),
                 "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1), "peak_source": peak_src}
+    traffic, tsrc = ncu_traffic(f"fused_kernel/{P}x{G}/{a.mode}/B{a.B}S{a.S}")
+    if traffic is not None:
+        roofline["traffic"] = traffic
+        roofline["traffic_source"] = tsrc
     if a.mode == "fused" and G > 1:
         # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
         # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)

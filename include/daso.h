@@ -258,11 +258,13 @@ daso_status daso_k_gather(const float* const* src, const size_t* numel, const si
 daso_status daso_k_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets,
                            int count, void* stream);
 
-/* Select how the fused update kernels (K1/K2/K3) move data; returns the previous
- * selection.  0 = register path (128-bit LDG/STG, grid-stride), 1 = TMA-staged path
- * (cp.async.bulk global<->shared through an mbarrier ring, one persistent CTA per SM).
+/* Select how the fused kernels move data; returns the previous selection.
+ * 0 = register path everywhere (128-bit LDG/STG), 1 = TMA-staged path everywhere
+ * (cp.async.bulk global<->shared through an mbarrier ring, one persistent CTA per SM;
+ * for the fused peer kernel the bulk copies read and write NVLink peer memory),
+ * 2 = auto (default): register path for the local kernels, TMA for the peer kernel.
  * Identical arithmetic in the same order: results are bit-identical.  Any other value
- * only queries.  Process-wide; default from the environment (DASO_KERNEL=ldg|tma). */
+ * only queries.  Process-wide; default from the environment (DASO_KERNEL=ldg|tma|auto). */
 int daso_kernel_impl(int impl);
 
 /* Order-independent 64-bit checksum of the bit patterns of x[n] (sum of the uint32

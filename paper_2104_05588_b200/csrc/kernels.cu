@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_kernel(const KernelArgs a,
     for (int64_t k = 0; k < my; ++k) {
         const int s = int(k % NS);
         unsigned char* st = smem + size_t(s) * L.bytes;
-        mbar_wait(&full[s], uint32_t((k / NS) & 1));
+        mbar_wait(&full[s], uint32_t((k / NS) & 1), a.flag);
         const int i = threadIdx.x * kVec;
         float* xs = reinterpret_cast<float*>(st + L.x) + i;
         float* vs = reinterpret_cast<float*>(st + L.v) + i;
@@ -258,12 +258,16 @@ int launch_t(const KernelArgs& a, cudaStream_t s) {
     return int(cudaGetLastError());
 }
 
-int g_impl = -1;   // 0 = register (LDG) path, 1 = TMA-staged path; default from DASO_KERNEL=ldg|tma
+// 0 = register (LDG) path everywhere, 1 = TMA-staged path everywhere, 2 = auto (default):
+// the measured-faster path per kernel — register path for the local fused kernels (one-shot
+// grid: ~100% of the copy peak), TMA for the NVLink peer kernel (0.77 vs 0.64 of the link
+// peak on B200, profiles/r01).  Default from DASO_KERNEL=ldg|tma|auto.
+int g_impl = -1;
 
 int kernel_impl() {
     if (g_impl < 0) {
         const char* e = getenv("DASO_KERNEL");
-        g_impl = (e && strcmp(e, "tma") == 0) ? 1 : 0;
+        g_impl = (e && strcmp(e, "tma") == 0) ? 1 : (e && strcmp(e, "ldg") == 0) ? 0 : 2;
     }
     return g_impl;
 }
@@ -386,7 +390,7 @@ int current_kernel_impl() { return kernel_impl(); }
 
 int set_kernel_impl(int impl) {
     const int prev = kernel_impl();
-    if (impl == 0 || impl == 1) g_impl = impl;
+    if (impl == 0 || impl == 1 || impl == 2) g_impl = impl;
     return prev;
 }
 

@@ -40,11 +40,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 // Spin until *p >= v.  A peer that never arrives (crashed process, protocol bug) must not
 // hang the GPU: after kBarrierTimeoutNs the wait gives up and raises bit 1 of the flag,
@@ -237,7 +232,7 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     for (int64_t k = 0; k < my; ++k) {
         const int s = int(k % NS);
         unsigned char* st = smem + size_t(s) * L.bytes;
-        mbar_wait(&full[s], uint32_t((k / NS) & 1));
+        mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err);
         const int i = threadIdx.x * 8;
         float x[8], v[8], g[8];
         Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
@@ -333,7 +328,7 @@ template <int OPS, int WIRE, int G>
 int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
     const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
                       reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
-    if (current_kernel_impl() == 1 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
+    if (current_kernel_impl() != 0 && al && pa.a.n >= kPT)   // TMA unless the register path is forced return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
     return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
 }
 

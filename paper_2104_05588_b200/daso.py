@@ -316,8 +316,8 @@ def daso_k_scatter(src, tensors, offsets, stream=None):
 
 
 def daso_kernel_impl(impl: int | str | None = None) -> int:
-    """Select the fused-kernel data path: 0/"ldg" or 1/"tma"; returns the previous one."""
-    code = {"ldg": 0, "tma": 1, None: -1}.get(impl, impl)
+    """Select the fused-kernel data path: 0/"ldg", 1/"tma", 2/"auto"; returns the previous one."""
+    code = {"ldg": 0, "tma": 1, "auto": 2, None: -1}.get(impl, impl)
     return int(lib().daso_kernel_impl(int(code)))
 
 

@@ -27,7 +27,7 @@ def parse(argv=None):
     ap.add_argument("--G", type=int, default=2)
     ap.add_argument("--B", type=int, default=4)
     ap.add_argument("--S", type=int, default=1)
-    ap.add_argument("--d", type=int, default=1000)
+    ap.add_argument("--dim", dest="d", type=int, default=1000)
     ap.add_argument("--b", type=int, default=32)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--lr", type=float, default=0.01)

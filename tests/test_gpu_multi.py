@@ -169,7 +169,7 @@ def test_world4_full_schedule(tmp_path, mode):
 def test_fused_tma_path_bit_identical(tmp_path, P, G):
     """The TMA-staged fused kernel (bulk copies over NVLink) computes exactly what the
     register-path fused kernel computes; d = 8192 spans several 2048-element tiles."""
-    args = TOY + ["--P", str(P), "--G", str(G), "--mode", "fused", "--d", "8192", "--steps", "12"]
+    args = TOY + ["--P", str(P), "--G", str(G), "--mode", "fused", "--dim", "8192", "--steps", "12"]
     a = run_world(str(tmp_path / "a"), 4, args + ["--kernel", "ldg"])
     b = run_world(str(tmp_path / "b"), 4, args + ["--kernel", "tma"])
     for ra, rb in zip(a, b):

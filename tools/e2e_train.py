@@ -1,9 +1,17 @@
 #!/usr/bin/env python
-"""End-to-end ResNet-50 training throughput on synthetic ImageNet-shaped batches
-(SURVEY §8(d) config 3): DASO through libdaso.so vs a synchronous all-reduce
-(the same library with one virtual node, P = 1, G = W) vs torch DDP + torch SGD.
+"""End-to-end training throughput on synthetic batches shaped like the paper's two
+workloads: ResNet-50 / ImageNet 224x224 and a hierarchical
+multi-scale attention segmentation net / Cityscapes 1024x2048 (config 4).
+DASO through libdaso.so vs a synchronous all-reduce (the same library with one
+virtual node, P = 1, G = W) vs torch DDP + torch SGD.
 
-    torchrun --nproc-per-node N tools/resnet_e2e.py --impl daso|sync|ddp [--batch 256]
+    torchrun --nproc-per-node N tools/e2e_train.py --model resnet50|hmsa --impl daso|sync|ddp
+
+HMSA stand-in (HRNet-OCR has no code or weights here): Tao et al.'s hierarchical
+multi-scale attention on a DeepLabV3-ResNet-50 trunk — the shared trunk + head predict
+at scales 0.5 and 1.0, an attention head on the 0.5-scale features weights the two
+(p = a * up(p_0.5) + (1 - a) * p_1.0), 19 classes, cross-entropy, batch-norm
+synchronised within the node-local process group.
 
 Model: torchvision resnet50 (25,557,032 params, 161 tensors), random init,
 channels_last, bf16 autocast for forward/backward only; fp32 master params,
@@ -26,13 +34,43 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def HMSA(classes: int):
+    import torch
+    import torch.nn.functional as F
+    import torchvision
+
+    class _HMSA(torch.nn.Module):
+        def __init__(self):
+            super().__init__()
+            seg = torchvision.models.segmentation.deeplabv3_resnet50(weights=None, weights_backbone=None,
+                                                                     num_classes=classes, aux_loss=False)
+            self.backbone, self.head = seg.backbone, seg.classifier
+            self.attn = torch.nn.Sequential(torch.nn.Conv2d(2048, 256, 3, padding=1, bias=False),
+                                            torch.nn.BatchNorm2d(256), torch.nn.ReLU(inplace=True),
+                                            torch.nn.Conv2d(256, 1, 1), torch.nn.Sigmoid())
+
+        def forward(self, x):
+            lo = F.interpolate(x, scale_factor=0.5, mode="bilinear", align_corners=False)
+            f_lo = self.backbone(lo)["out"]
+            p_lo, att = self.head(f_lo), self.attn(f_lo)
+            p_hi = self.head(self.backbone(x)["out"])
+            size = p_hi.shape[-2:]
+            p = F.interpolate(att * p_lo, size=size, mode="bilinear", align_corners=False) + \
+                (1 - F.interpolate(att, size=size, mode="bilinear", align_corners=False)) * p_hi
+            return F.interpolate(p, size=x.shape[-2:], mode="bilinear", align_corners=False)
+
+    return _HMSA()
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--model", choices=["resnet50", "hmsa"], default="resnet50")
     ap.add_argument("--impl", choices=["daso", "sync", "ddp"], default="daso")
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default 256 resnet50, 2 hmsa)")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--gpus-per-node", type=int, default=0, help="DASO G (default: 2 if world >= 4 else 1)")
+    ap.add_argument("--gpus-per-node", type=int, default=0,
+                    help="DASO G (default: 2 if world >= 4 else 1); also the node group of SyncBN")
     ap.add_argument("--mode", default="faithful")
     ap.add_argument("--lr", type=float, default=0.1)
     a = ap.parse_args()
@@ -48,11 +86,29 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("gloo")
+    G_node = a.gpus_per_node or (2 if world >= 4 else 1)
+    if a.impl == "sync":
+        G_node = world
+    if a.impl == "ddp":
+        G_node = min(G_node, world)
     torch.manual_seed(0)                       # identical init on every rank (R17)
-    model = torchvision.models.resnet50().to(dev).to(memory_format=torch.channels_last)
     gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    images = torch.randn(a.batch, 3, 224, 224, device=dev, generator=gen).to(memory_format=torch.channels_last)
-    labels = torch.randint(0, 1000, (a.batch,), device=dev, generator=gen)
+    if a.model == "resnet50":
+        a.batch = a.batch or 256
+        model = torchvision.models.resnet50()
+        images = torch.randn(a.batch, 3, 224, 224, device=dev, generator=gen)
+        labels = torch.randint(0, 1000, (a.batch,), device=dev, generator=gen)
+    else:
+        a.batch = a.batch or 2
+        model = HMSA(19)
+        images = torch.randn(a.batch, 3, 1024, 2048, device=dev, generator=gen)
+        labels = torch.randint(0, 19, (a.batch, 1024, 2048), device=dev, generator=gen)
+        if world > 1:   # node-local SyncBN
+            groups = [dist.new_group(list(range(j * G_node, (j + 1) * G_node)), backend="nccl")
+                      for j in range(world // G_node)]
+            model = torch.nn.SyncBatchNorm.convert_sync_batchnorm(model, process_group=groups[rank // G_node])
+    model = model.to(dev).to(memory_format=torch.channels_last)
+    images = images.to(memory_format=torch.channels_last)
     loss_fn = torch.nn.CrossEntropyLoss()
 
     ctx = None
@@ -68,7 +124,7 @@ def main():
         if a.impl == "sync":
             P, G, B, S = 1, world, 1, 0
         else:
-            G = a.gpus_per_node or (2 if world >= 4 else 1)
+            G = G_node
             P, B, S = world // G, 4, 1
         uid = daso.rendezvous_unique_id() if world > 1 else daso.daso_get_unique_id()
         ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
@@ -110,7 +166,9 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    out = {"workload": "resnet50 synthetic 224x224 (config 3)", "impl": a.impl, "n_gpus": world,
+    wl = {"resnet50": "resnet50 synthetic 224x224 (config 3)",
+          "hmsa": "hierarchical multi-scale attention seg. synthetic 1024x2048, 19 classes (config 4)"}[a.model]
+    out = {"workload": wl, "impl": a.impl, "n_gpus": world, "params": sum(p.numel() for p in model.parameters()),
            "batch_per_gpu": a.batch, "steps": a.steps, "ms_per_step": ms / a.steps,
            "samples_per_s": a.batch * world * a.steps / (ms * 1e-3), "loss": float(loss.item())}
     if ctx is not None:
