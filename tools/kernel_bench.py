@@ -3,9 +3,9 @@
 
     python tools/kernel_bench.py [--n 25557032] [--iters 50] [--only K1,K3]
 
-Each kernel is launched through the C ABI (daso_k_*) on resident buffers larger
-than L2 (every launch streams >= 150 MB), timed with CUDA events on the launching
-stream over `iters` back-to-back launches after 5 warm-up launches.  achieved =
+Each kernel is launched through the C ABI (daso_k_*) on resident buffers, timed
+with CUDA events on the launching stream around each launch; between launches a
+256 MB buffer is read (untimed) so every launch starts from a cold, clean L2.  achieved =
 algorithmic bytes per launch / mean launch time.  Also the target
 command for `ncu --set full` (use --iters 3).
 """
@@ -55,6 +55,7 @@ def main():
     xs = x[:n]
     # restrict to n elements (the ABI takes numel from x)
     x, v, g = x[:n], v[:n], g[:n]
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")   # 256 MB > 126 MB L2
     only = set(a.only.split(",")) if a.only else None
     rows = {}
     for name, (fn, bpp) in cases.items():
@@ -63,13 +64,14 @@ def main():
         for _ in range(a.warmup):
             fn()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.iters):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.iters)]
+        for e0, e1 in ev:
+            flush.sum()                 # evict L2 with clean lines (untimed; no dirty write-back to pay)
+            e0.record()
             fn()
-        e1.record()
+            e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.iters
+        ms = sum(e0.elapsed_time(e1) for e0, e1 in ev) / a.iters
         gbs = bpp * n / (ms * 1e-3) / 1e9
         rows[name] = {"bytes_per_param": bpp, "us": ms * 1e3, "GB/s": gbs, "frac_of_measured_peak": gbs / peak}
     del xs
