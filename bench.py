@@ -12,12 +12,19 @@ Workload: n = 25,557,032 fp32 parameters (ResNet-50-sized), synthetic seeded
 gradients, B = 4, S = 1, topology P x G virtual nodes: N=1 -> 1x1,
 2 -> 2x1, 4 -> 2x2, 8 -> 2x4.
 
+Mode: default "fused" — the node tier (gradient reduce over the node's
+GPUs + update/merge/pack + parameter all-gather) in one kernel over NVLink peer
+memory; "faithful" = the paper's structure (node all-reduce, rotating group exchange,
+node broadcast); "sharded" = the same with NCCL reduce-scatter / all-gather.  All
+three are parity-tested against the oracle.
+
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the
-compute stream (the stream daso_step runs on); the gradient bucket is refreshed
-from a resident copy between steps outside the events (a backward pass would
+compute stream (the stream daso_step runs on).  Between steps, outside the events,
+the gradient bucket is refreshed from a resident copy (a backward pass would
 overwrite it; without the refresh the node all-reduce would grow it G-fold per
-step).  Barrier + synchronize on both sides; max over ranks.  value = fp32
-parameter bytes synchronised per second over all ranks = 4 n N / t_step.
+step) and L2 is flushed by reading a 256 MB buffer.  Barrier + synchronize on both
+sides; max over ranks.  value = fp32 parameter bytes synchronised per second over
+all ranks = 4 n N / t_step.
 """
 from __future__ import annotations
 
@@ -47,7 +54,7 @@ def parse():
     ap.add_argument("--S", type=int, default=1)
     ap.add_argument("--n", type=int, default=N_PARAMS)
     ap.add_argument("--topology", default="", help="PxG, default by --gpus")
-    ap.add_argument("--mode", choices=["faithful", "sharded", "fused"], default="faithful")
+    ap.add_argument("--mode", choices=["faithful", "sharded", "fused"], default="fused")
     ap.add_argument("--wire", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")

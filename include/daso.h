@@ -192,6 +192,18 @@ daso_status daso_global_merge(daso_ctx* c, void* stream);
  * `plateau` as in daso_sched_next. */
 daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out);
 
+/* ----- backward-overlapped local sync ("The local networks utilize
+ * PyTorch's DistributedDataParallel") -----
+ * daso_local_sync_bucket: node all-reduce (sum) of g[offset, offset + count) on a dedicated
+ *   node communicator, enqueued on `stream` (typically a comm stream fed by gradient-ready
+ *   hooks during backward).  Every rank must issue the same buckets in the same order.
+ *   Faithful mode only (DASO_ERR_PROTOCOL otherwise); DASO_ERR_RANGE outside [0, n).
+ * daso_step_ex: daso_step with flags; DASO_STEP_GRADS_REDUCED = g already holds the node
+ *   sum (the buckets covered [0, n) and `stream` waits on them): skip the node all-reduce. */
+enum { DASO_STEP_GRADS_REDUCED = 1 };
+daso_status daso_local_sync_bucket(daso_ctx* c, size_t offset, size_t count, void* stream);
+daso_status daso_step_ex(daso_ctx* c, float lr, int plateau, int flags, void* stream, daso_record* out);
+
 /* daso_step_host: daso_step fed from HOST memory: copies host_grads[n] (pinned
  * for async) into the bound g on `stream`, runs daso_step, then copies the 4-byte
  * non-finite flag back into *host_flag (if non-null) and synchronises `stream`. */

@@ -17,6 +17,7 @@ OK, ERR_CONFIG, ERR_RANGE, ERR_PROTOCOL, ERR_ARGUMENT, ERR_CUDA, ERR_NCCL, ERR_N
 WARMUP, CYCLING, COOLDOWN = 0, 1, 2
 WIRE_BF16, WIRE_FP32 = 0, 1
 MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED = 0, 1, 2
+STEP_GRADS_REDUCED = 1
 
 
 class SchedConfig(C.Structure):
@@ -86,6 +87,8 @@ _SIG = {
     "daso_global_send": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "daso_global_merge": (C.c_int, [C.c_void_p, C.c_void_p]),
     "daso_step": (C.c_int, [C.c_void_p, C.c_float, C.c_int, C.c_void_p, C.POINTER(Record)]),
+    "daso_step_ex": (C.c_int, [C.c_void_p, C.c_float, C.c_int, C.c_int, C.c_void_p, C.POINTER(Record)]),
+    "daso_local_sync_bucket": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p]),
     "daso_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_float, C.c_int, C.c_void_p, C.POINTER(Record),
                                  C.POINTER(C.c_uint32)]),
     "daso_query": (C.c_int, [C.c_void_p, C.POINTER(Record)]),

@@ -34,6 +34,7 @@ struct daso_ctx {
     daso::Schedule* sched = nullptr;
 
     ncclComm_t world_comm = nullptr, node_comm = nullptr, group_comm = nullptr;
+    ncclComm_t bucket_comm = nullptr;   // node comm for backward-overlapped bucket all-reduces (N2)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
 
@@ -106,7 +107,7 @@ ncclDataType_t wire_nccl(int wire) { return wire == DASO_WIRE_BF16 ? ncclBfloat1
 daso_status poll_async(daso_ctx* c) {
     cudaError_t e = cudaPeekAtLastError();
     if (e != cudaSuccess) return c->fail(DASO_ERR_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(e));
-    ncclComm_t comms[3] = {c->world_comm, c->node_comm, c->group_comm};
+    ncclComm_t comms[4] = {c->world_comm, c->node_comm, c->group_comm, c->bucket_comm};
     for (ncclComm_t m : comms) {
         if (!m) continue;
         ncclResult_t a = ncclSuccess;
@@ -221,9 +222,9 @@ daso_status node_bcast(daso_ctx* c, int root, cudaStream_t s) {
 }
 
 // ---- faithful (v1) batch ---------------------------------------------------------
-daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s) {
+daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStream_t s, bool reduced) {
     const bool global = c->P > 1;
-    if (c->G > 1) {   // Fig. 2: node-local gradient sum (x 1/G in the kernel)
+    if (c->G > 1 && !reduced) {   // Fig. 2: node-local gradient sum (x 1/G in the kernel)
         Span sp(c, s, PH_LOCAL, 2.0 * (c->G - 1) / c->G * 4.0 * double(c->n));
         NCCL_TRY(c, ncclAllReduce(c->g, c->g, size_t(c->n), ncclFloat32, ncclSum, c->node_comm, s));
     }
@@ -544,6 +545,9 @@ daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S
         gc.minCTAs = 1;
     }
     NCCL_TRY(c, ncclCommSplit(c->world_comm, c->local, c->node, &c->group_comm, &gc));
+    ncclConfig_t bc = NCCL_CONFIG_INITIALIZER;
+    bc.blocking = 1;
+    NCCL_TRY(c, ncclCommSplit(c->world_comm, c->node, c->local, &c->bucket_comm, &bc));
 
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -649,9 +653,26 @@ daso_status daso_global_merge(daso_ctx* c, void* stream) {
     return DASO_OK;
 }
 
-daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out) {
+daso_status daso_local_sync_bucket(daso_ctx* c, size_t offset, size_t count, void* stream) {
     if (!c) return DASO_ERR_ARGUMENT;
     STATUS_TRY(require_bound(c));
+    if (c->cfg.mode != DASO_MODE_FAITHFUL)
+        return c->fail(DASO_ERR_PROTOCOL, "bucketed local sync requires DASO_MODE_FAITHFUL");
+    if (offset > size_t(c->n) || count > size_t(c->n) - offset)
+        return c->fail(DASO_ERR_RANGE, "bucket [%zu, %zu) outside [0, %lld)", offset, offset + count, (long long)c->n);
+    if (c->G == 1 || count == 0) return DASO_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    Span sp(c, s, PH_LOCAL, 2.0 * (c->G - 1) / c->G * 4.0 * double(count));
+    NCCL_TRY(c, ncclAllReduce(c->g + offset, c->g + offset, count, ncclFloat32, ncclSum, c->bucket_comm, s));
+    return DASO_OK;
+}
+
+daso_status daso_step_ex(daso_ctx* c, float lr, int plateau, int flags, void* stream, daso_record* out) {
+    if (!c) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    const bool reduced = (flags & DASO_STEP_GRADS_REDUCED) != 0;
+    if (reduced && c->cfg.mode != DASO_MODE_FAITHFUL)
+        return c->fail(DASO_ERR_PROTOCOL, "DASO_STEP_GRADS_REDUCED requires DASO_MODE_FAITHFUL");
     const daso_record r = c->sched->next(plateau);
     c->last = r;
     if (c->tracing) c->acc.steps += 1;
@@ -661,7 +682,11 @@ daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_rec
         return c->fail(DASO_ERR_PROTOCOL, "schedule merge at step %lld but nothing in flight", (long long)r.step);
     if (c->cfg.mode == DASO_MODE_SHARDED) return step_sharded(c, r, lr, s);
     if (c->cfg.mode == DASO_MODE_FUSED) return step_fused(c, r, lr, s);
-    return step_faithful(c, r, lr, s);
+    return step_faithful(c, r, lr, s, reduced);
+}
+
+daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out) {
+    return daso_step_ex(c, lr, plateau, 0, stream, out);
 }
 
 daso_status daso_step_host(daso_ctx* c, const float* host_grads, float lr, int plateau, void* stream,
@@ -748,7 +773,7 @@ daso_status daso_finalize(daso_ctx* c) {
         for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
         if (c->sig) cudaFree(c->sig);
     }
-    ncclComm_t comms[3] = {c->group_comm, c->node_comm, c->world_comm};
+    ncclComm_t comms[4] = {c->bucket_comm, c->group_comm, c->node_comm, c->world_comm};
     for (ncclComm_t m : comms) {
         if (!m) continue;
         if (ncclCommFinalize(m) != ncclSuccess) st = DASO_ERR_NCCL;

@@ -157,6 +157,16 @@ class Ctx:
         self._check(lib().daso_step(self._h, float(lr), int(plateau), _stream(stream), C.byref(r)), "daso_step")
         return r.as_dict()
 
+    def step_ex(self, lr: float, plateau: int = 0, grads_reduced: bool = False, stream=None) -> dict:
+        r = Record()
+        self._check(lib().daso_step_ex(self._h, float(lr), int(plateau), L.STEP_GRADS_REDUCED if grads_reduced else 0,
+                                       _stream(stream), C.byref(r)), "daso_step_ex")
+        return r.as_dict()
+
+    def local_sync_bucket(self, offset: int, count: int, stream=None):
+        self._check(lib().daso_local_sync_bucket(self._h, int(offset), int(count), _stream(stream)),
+                    "daso_local_sync_bucket")
+
     def step_host(self, host_grads, lr: float, plateau: int = 0, stream=None) -> tuple[dict, int]:
         """host_grads: a (pinned) CPU float32 tensor of n elements."""
         torch = _torch()
@@ -324,6 +334,70 @@ def daso_kernel_impl(impl: int | str | None = None) -> int:
 def daso_k_checksum(x, out_u64, stream=None):
     """out_u64: a 1-element int64 CUDA tensor receiving the checksum bits."""
     check(lib().daso_k_checksum(_ptr(x), x.numel(), _ptr(out_u64), _stream(stream)), "daso_k_checksum")
+
+
+# ------------------------------------------------------------------ backward-overlapped local sync
+class OverlappedLocalSync:
+    """Bucketed node all-reduce overlapped with backward (the DDP
+    behaviour of the paper's local tier).  Buckets are contiguous ranges of the
+    flat gradient bucket in reverse parameter order (~bucket_mb each); a post-accumulate
+    grad hook launches a bucket's all-reduce (daso_local_sync_bucket) on a comm stream as
+    soon as all its gradients exist.  Call ``step(lr)`` after backward: the compute stream
+    waits for the buckets and runs daso_step_ex(..., grads_reduced=True)."""
+
+    def __init__(self, ctx: Ctx, flat: "FlatParams", bucket_mb: float = 25.0):
+        torch = _torch()
+        self.ctx, self.flat = ctx, flat
+        self.stream = torch.cuda.Stream(priority=-1)
+        limit = int(bucket_mb * (1 << 20) / 4)
+        order = list(range(len(flat.params)))[::-1]            # backward produces grads ~ in reverse
+        self.buckets, cur = [], []
+        for i in order:
+            cur.append(i)
+            lo = flat.offsets[cur[-1]]
+            hi = flat.offsets[cur[0]] + flat.params[cur[0]].numel()
+            if hi - lo >= limit:
+                self.buckets.append(cur)
+                cur = []
+        if cur:
+            self.buckets.append(cur)
+        self.ranges = []
+        for b in self.buckets:
+            lo = flat.offsets[b[-1]]
+            hi = flat.offsets[b[0]] + flat.params[b[0]].numel() if b[0] == len(flat.params) - 1 else flat.offsets[b[0] + 1]
+            self.ranges.append((lo, min(hi, flat.n) - lo))
+        self.bucket_of = {i: k for k, b in enumerate(self.buckets) for i in b}
+        self.pending = [len(b) for b in self.buckets]
+        self.launched = 0
+        self.handles = [p.register_post_accumulate_grad_hook(self._hook(i)) for i, p in enumerate(flat.params)]
+
+    def _hook(self, i):
+        def fn(_p):
+            k = self.bucket_of[i]
+            self.pending[k] -= 1
+            if self.pending[k] == 0:
+                torch = _torch()
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream())
+                self.stream.wait_event(ev)
+                self.ctx.local_sync_bucket(*self.ranges[k], stream=self.stream)
+                self.launched += 1
+        return fn
+
+    def step(self, lr: float, plateau: int = 0) -> dict:
+        torch = _torch()
+        if self.launched != len(self.buckets):
+            raise RuntimeError(f"only {self.launched} of {len(self.buckets)} gradient buckets became ready")
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        torch.cuda.current_stream().wait_event(ev)
+        self.pending = [len(b) for b in self.buckets]
+        self.launched = 0
+        return self.ctx.step_ex(lr, plateau, grads_reduced=True)
+
+    def remove(self):
+        for h in self.handles:
+            h.remove()
 
 
 # ------------------------------------------------------------------ flat buckets for a torch model

@@ -175,3 +175,26 @@ def test_fused_tma_path_bit_identical(tmp_path, P, G):
     for ra, rb in zip(a, b):
         np.testing.assert_array_equal(ra["trace"].view(np.uint32), rb["trace"].view(np.uint32))
     check(b, P, G, 4, 1, steps=12, d=8192)
+
+
+@pytest.mark.parametrize("world,G", [(2, 2), (4, 2), (4, 4)])
+def test_backward_overlapped_local_sync(tmp_path, world, G):
+    """N2: bucketed node all-reduce launched from gradient hooks during backward
+    (OverlappedLocalSync + daso_step_ex(grads_reduced)) gives the same training
+    trajectory as the all-reduce inside daso_step (bitwise for 2-GPU nodes, where a
+    sum of two is order-free; fp32 rounding of the reduction order otherwise)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    out = str(tmp_path / "out")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_overlap.py"),
+           "--G", str(G), "--out", out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    for i in range(world):
+        f = np.load(os.path.join(out, f"rank{i}.npz"))
+        assert int(f["n_buckets"]) > 1
+        if G == 2:
+            np.testing.assert_array_equal(f["plain"].view(np.uint32), f["overlap"].view(np.uint32))
+        else:
+            np.testing.assert_allclose(f["overlap"], f["plain"], rtol=1e-5, atol=1e-6)

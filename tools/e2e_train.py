@@ -73,6 +73,8 @@ def main():
                     help="DASO G (default: 2 if world >= 4 else 1); also the node group of SyncBN")
     ap.add_argument("--mode", default="faithful")
     ap.add_argument("--lr", type=float, default=0.1)
+    ap.add_argument("--overlap", action="store_true",
+                    help="faithful mode: node all-reduce in buckets overlapped with backward (N2)")
     a = ap.parse_args()
 
     import torch
@@ -131,6 +133,7 @@ def main():
                              total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode)
         flat = daso.FlatParams(model.parameters(), gpus_per_node=G)
         ctx.bind(flat.x, flat.g, flat.v, flat.n)
+        overlap = daso.OverlappedLocalSync(ctx, flat) if a.overlap else None
         net = model
 
     def step():
@@ -143,6 +146,8 @@ def main():
         loss.backward()
         if ctx is None:
             opt.step()
+        elif overlap is not None:
+            overlap.step(a.lr)
         else:
             ctx.step(a.lr)
         return loss
@@ -174,7 +179,7 @@ def main():
     if ctx is not None:
         tr = ctx.trace_read(reset=True)
         sync_ms = (tr["kernel_ms"] + tr["local_ms"] + tr["node_ms"] + tr["wait_ms"]) / a.steps
-        out.update({"topology": f"{ctx.P}x{ctx.G}", "mode": a.mode, "sync_path_ms_per_step": sync_ms,
+        out.update({"topology": f"{ctx.P}x{ctx.G}", "mode": a.mode, "overlap": a.overlap, "sync_path_ms_per_step": sync_ms,
                     "sync_share": sync_ms / (ms / a.steps), "finite": ctx.check_finite()})
         ctx.finalize()
     if rank == 0:
