@@ -168,8 +168,9 @@ int launch_peer_t(const PeerArgs& pa, cudaStream_t s, int sms) {
 // to G peers (G-1 remote), v and the packed row out locally.
 constexpr int kPT = 2048;
 
-struct PeerTmaLayout {
-    uint32_t x, v, g, slot, pack, bytes;
+struct PeerTmaLayout {   // byte offsets: NS input stages, then NO output buffers, then NS mbarriers
+    uint32_t x, v, g, slot, in_bytes;    // inside an input stage
+    uint32_t ox, ov, opack, out_bytes;   // inside an output buffer
 };
 __host__ __device__ inline PeerTmaLayout peer_tma_layout(int ops, int G, int P, int wb) {
     PeerTmaLayout L{};
@@ -178,20 +179,28 @@ __host__ __device__ inline PeerTmaLayout peer_tma_layout(int ops, int G, int P, 
     L.v = o; o += kPT * 4;
     L.g = o; o += uint32_t(G) * kPT * 4;
     L.slot = o; if (ops & OP_MERGE) o += uint32_t(P) * kPT * wb;
-    L.pack = o; if (ops & OP_PACK) o += kPT * wb;
-    L.bytes = (o + 127) / 128 * 128;
+    L.in_bytes = (o + 127) / 128 * 128;
+    o = 0;
+    L.ox = o; o += kPT * 4;
+    L.ov = o; o += kPT * 4;
+    L.opack = o; if (ops & OP_PACK) o += kPT * wb;
+    L.out_bytes = (o + 127) / 128 * 128;
     return L;
 }
+constexpr int kPeerOut = 2;   // output buffers (double-buffered bulk stores)
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+// Input stage s is refilled as soon as its tile has been computed (outputs go to a separate
+// double-buffered output area), so the loads never wait for the NVLink stores to drain.
 template <int OPS, int WIRE, int G>
 __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArgs pa, int NS) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
     const KernelArgs& a = pa.a;
     const PeerTmaLayout L = peer_tma_layout(OPS, G, a.P, wb);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * L.bytes);
+    unsigned char* outs = smem + size_t(NS) * L.in_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(kPeerOut) * L.out_bytes);
     const bool leader = threadIdx.x == 0;
     // 1. start barrier
     if (blockIdx.x == 0 && threadIdx.x < G) {
@@ -210,15 +219,15 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     auto issue_load = [&](int64_t k) {
         const int s = int(k % NS);
-        unsigned char* st = smem + size_t(s) * L.bytes;
+        unsigned char* st = smem + size_t(s) * L.in_bytes;
         const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kPT;
         uint32_t tx = (2u + G) * kPT * 4u;
         if constexpr ((OPS & OP_MERGE) != 0) tx += uint32_t(a.P) * kPT * wb;
         mbar_expect_tx(&full[s], tx);
-        bulk_g2s(st + L.x, a.x + e0, kPT * 4, &full[s]);
-        bulk_g2s(st + L.v, a.v + e0, kPT * 4, &full[s]);
 #pragma unroll
         for (int q = 0; q < G; ++q) bulk_g2s(st + L.g + uint32_t(q) * kPT * 4, pa.gp[q] + e0, kPT * 4, &full[s]);
+        bulk_g2s(st + L.x, a.x + e0, kPT * 4, &full[s]);
+        bulk_g2s(st + L.v, a.v + e0, kPT * 4, &full[s]);
         if constexpr ((OPS & OP_MERGE) != 0) {
             for (int p = 0; p < a.P; ++p)
                 bulk_g2s(st + L.slot + uint32_t(p) * kPT * wb,
@@ -231,8 +240,11 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     bool bad = false;
     for (int64_t k = 0; k < my; ++k) {
         const int s = int(k % NS);
-        unsigned char* st = smem + size_t(s) * L.bytes;
+        unsigned char* st = smem + size_t(s) * L.in_bytes;
+        unsigned char* ob = outs + size_t(k % kPeerOut) * L.out_bytes;
+        if (leader && k >= kPeerOut) bulk_wait_read<kPeerOut - 1>();   // output buffer ob drained
         mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err);
+        __syncthreads();                                                 // also publishes the drain
         const int i = threadIdx.x * 8;
         float x[8], v[8], g[8];
         Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
@@ -264,25 +276,25 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
         }
-        Wire<DASO_WIRE_FP32>::template store_smem<8>(st + L.x, i, x);
-        Wire<DASO_WIRE_FP32>::template store_smem<8>(st + L.v, i, v);
-        if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(st + L.pack, i, x);
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
+        if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
 #pragma unroll
         for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
         fence_async_smem();
-        __syncthreads();
+        __syncthreads();                                                 // stage s consumed, ob written
         if (leader) {
+            if (k + NS < my) issue_load(k + NS);                         // refill stage s right away
             const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kPT;
-            bulk_s2g(a.v + e0, st + L.v, kPT * 4);
 #pragma unroll
-            for (int q = 0; q < G; ++q) bulk_s2g(pa.xp[q] + e0, st + L.x, kPT * 4);
-            if constexpr ((OPS & OP_PACK) != 0)
-                bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, st + L.pack, kPT * wb);
-            bulk_commit();
-            if (k >= 1 && k - 1 + NS < my) {
-                bulk_wait_read<1>();
-                issue_load(k - 1 + NS);
+            for (int q = 0; q < G; ++q) {                                // start with the next peer: spread links
+                const int qq = (pa.me + 1 + q) % G;
+                bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
             }
+            bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
+            if constexpr ((OPS & OP_PACK) != 0)
+                bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, ob + L.opack, kPT * wb);
+            bulk_commit();
         }
     }
     if (leader) bulk_wait_all();
@@ -311,15 +323,15 @@ template <int OPS, int WIRE, int G>
 int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
     const PeerTmaLayout L = peer_tma_layout(OPS, G, pa.a.P, wb);
-    const int budget = 200 * 1024;
-    const int NS = int(std::min<int64_t>(8, (budget - 64) / L.bytes));
+    const int budget = 210 * 1024 - kPeerOut * int(L.out_bytes);
+    const int NS = int(std::min<int64_t>(8, (budget - 64) / L.in_bytes));
     if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    const size_t smem = size_t(NS) * L.bytes + 8 * size_t(NS);
+    const size_t smem = size_t(NS) * L.in_bytes + size_t(kPeerOut) * L.out_bytes + 8 * size_t(NS);
     peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(sms)), dim3(kPeerThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
 }

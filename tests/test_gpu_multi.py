@@ -198,3 +198,36 @@ def test_backward_overlapped_local_sync(tmp_path, world, G):
             np.testing.assert_array_equal(f["plain"].view(np.uint32), f["overlap"].view(np.uint32))
         else:
             np.testing.assert_allclose(f["overlap"], f["plain"], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("mode,wire", [("fused", "bf16"), ("faithful", "bf16"), ("sharded", "bf16"),
+                                       ("fused", "fp32")])
+def test_full_size_microbench_sampled(tmp_path, mode, wire):
+    """Full BASELINE size (n = 25,557,032, 2x2, B=4, S=1, bf16 wire), bench.py's launch
+    configuration, 8 steps (two merges): 20,004 sampled parameters of every rank against
+    the oracle simulating exactly those elements (the method is elementwise given the
+    gradients, so the sample is the oracle's full answer for those indices)."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    sys.path.insert(0, HERE)
+    import mp_micro
+    out = str(tmp_path / "out")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_micro.py"),
+           "--G", "2", "--mode", mode, "--wire", wire, "--out", out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    idx = mp_micro.sample_indices()
+    N = mp_micro.N
+    grads = {(rk, k): synthetic.microbench_grad(N, rk, k)[idx] for rk in range(4) for k in range(8)}
+    cfg = SchedConfig(B_init=4, S_init=1, total_epochs=1, steps_per_epoch=4 << 20)
+    ref = daso_sim.simulate(2, 2, cfg, 8, synthetic.microbench_x0(N)[idx], lambda rk, k, w: grads[(rk, k)],
+                            0.1, 0.9, 1e-4, wire=wire, trace=True)
+    tol = 1e-2 if wire == "bf16" else 1e-5
+    for rk in range(4):
+        tr = np.load(os.path.join(out, f"rank{rk}.npz"))["trace"].astype(np.float64)
+        for k in range(8):
+            xo = ref["trace"][k][rk]
+            rms = np.sqrt(np.mean(xo ** 2))
+            assert np.all(np.abs(tr[k] - xo) <= tol * (np.abs(xo) + rms)), (rk, k)
+            assert np.linalg.norm(tr[k] - xo) <= tol * np.linalg.norm(xo)
