@@ -48,12 +48,20 @@ def run_world(tmp, world, args):
         a = mp_toy.parse([*args, "--out", out])
         run_torch_single(mp_toy, a)
     else:
-        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_toy.py"),
-               *args, "--out", out]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+        torchrun(world, "mp_toy.py", [*args, "--out", out])
     return [np.load(os.path.join(out, f"rank{i}.npz")) for i in range(world)]
+
+
+def torchrun(world, script, args, timeout=600):
+    """Launch `script` on `world` GPUs; retry on a rendezvous-port collision (EADDRINUSE)."""
+    for _ in range(4):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, script), *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    return r
 
 
 def run_torch_single(mp_toy, a):
@@ -186,11 +194,7 @@ def test_backward_overlapped_local_sync(tmp_path, world, G):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     out = str(tmp_path / "out")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_overlap.py"),
-           "--G", str(G), "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    torchrun(world, "mp_overlap.py", ["--G", str(G), "--out", out])
     for i in range(world):
         f = np.load(os.path.join(out, f"rank{i}.npz"))
         assert int(f["n_buckets"]) > 1
@@ -212,11 +216,7 @@ def test_full_size_microbench_sampled(tmp_path, mode, wire):
     sys.path.insert(0, HERE)
     import mp_micro
     out = str(tmp_path / "out")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.join(HERE, "mp_micro.py"),
-           "--G", "2", "--mode", mode, "--wire", wire, "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-6000:]
+    torchrun(4, "mp_micro.py", ["--G", "2", "--mode", mode, "--wire", wire, "--out", out], timeout=900)
     idx = mp_micro.sample_indices()
     N = mp_micro.N
     grads = {(rk, k): synthetic.microbench_grad(N, rk, k)[idx] for rk in range(4) for k in range(8)}
