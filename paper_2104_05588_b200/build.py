@@ -55,7 +55,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nroot = nccl_root()
     objdir = os.path.join(PKG, "build")
     os.makedirs(objdir, exist_ok=True)
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall",
+              "-Werror", "all-warnings",
               "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nroot, "include")]
     objs = []
     for src in sources():

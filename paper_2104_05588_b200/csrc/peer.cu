@@ -340,7 +340,8 @@ template <int OPS, int WIRE, int G>
 int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
     const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
                       reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
-    if (current_kernel_impl() != 0 && al && pa.a.n >= kPT)   // TMA unless the register path is forced return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
+    // TMA unless the register path is forced (daso_kernel_impl(0))
+    if (current_kernel_impl() != 0 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
     return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
 }
 
