@@ -189,8 +189,9 @@ def test_fused_tma_path_bit_identical(tmp_path, P, G):
 def test_backward_overlapped_local_sync(tmp_path, world, G):
     """N2: bucketed node all-reduce launched from gradient hooks during backward
     (OverlappedLocalSync + daso_step_ex(grads_reduced)) gives the same training
-    trajectory as the all-reduce inside daso_step (bitwise for 2-GPU nodes, where a
-    sum of two is order-free; fp32 rounding of the reduction order otherwise)."""
+    trajectory as the all-reduce inside daso_step, to fp32 rounding (cuDNN's weight-
+    gradient kernels are not bitwise deterministic run to run, so two runs of the same
+    backward already differ in the last bits)."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     out = str(tmp_path / "out")
@@ -198,10 +199,7 @@ def test_backward_overlapped_local_sync(tmp_path, world, G):
     for i in range(world):
         f = np.load(os.path.join(out, f"rank{i}.npz"))
         assert int(f["n_buckets"]) > 1
-        if G == 2:
-            np.testing.assert_array_equal(f["plain"].view(np.uint32), f["overlap"].view(np.uint32))
-        else:
-            np.testing.assert_allclose(f["overlap"], f["plain"], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(f["overlap"], f["plain"], rtol=1e-5, atol=1e-7)
 
 
 @pytest.mark.parametrize("mode,wire", [("fused", "bf16"), ("faithful", "bf16"), ("sharded", "bf16"),
