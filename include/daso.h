@@ -247,6 +247,7 @@ daso_status daso_topology(const daso_ctx* c, int* P, int* G, int* node, int* loc
  *   + merge:      x = x + sum_{i<P} (wire_f32(slot[i]) - x) / (2S + P)   (K3, Eq. (1), delta form)
  *   + pack:       pack_out = wire(x)                                     (K2)
  *   average:      x = sum_{i<P} wire_f32(slot[i]) / P                    (K4, Fig. 3)
+ * n = 0 is a successful no-op (pointers are not inspected).
  * slot is P rows of `slot_stride` wire elements (row i = node i).  `wire` is
  * DASO_WIRE_BF16 (uint16 bf16 rows) or DASO_WIRE_FP32 (float rows).  flag (nullable)
  * gets bit 0 set if any written parameter is non-finite. */

@@ -799,6 +799,7 @@ static daso_status kstatus(int e) { return e == 0 ? DASO_OK : DASO_ERR_CUDA; }
 
 daso_status daso_k_update(float* x, float* v, const float* g, size_t n, float lr, float mu, float wd, float gscale,
                           void* pack_out, int wire, uint32_t* flag, void* stream) {
+    if (n == 0) return DASO_OK;   // empty bucket: nothing to do
     if (!x || !v || !g || !aligned16(x) || !aligned16(v) || !aligned16(g)) return DASO_ERR_ARGUMENT;
     if (pack_out && !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
     if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
@@ -817,6 +818,7 @@ static bool slot_ok(const void* slot, size_t stride, int P, int wire) {
 daso_status daso_k_update_merge(float* x, float* v, const float* g, size_t n, float lr, float mu, float wd,
                                 float gscale, const void* slot, size_t slot_stride, int P, int S, void* pack_out,
                                 int wire, uint32_t* flag, void* stream) {
+    if (n == 0) return DASO_OK;
     if (!x || !v || !g || !aligned16(x) || !aligned16(v) || !aligned16(g)) return DASO_ERR_ARGUMENT;
     if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
     if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n || S < 1) return DASO_ERR_ARGUMENT;
@@ -832,6 +834,7 @@ daso_status daso_k_update_merge(float* x, float* v, const float* g, size_t n, fl
 
 daso_status daso_k_merge(float* x, size_t n, const void* slot, size_t slot_stride, int P, int S, void* pack_out,
                          int wire, uint32_t* flag, void* stream) {
+    if (n == 0) return DASO_OK;
     if (!x || !aligned16(x)) return DASO_ERR_ARGUMENT;
     if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
     if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n || S < 1) return DASO_ERR_ARGUMENT;
@@ -845,6 +848,7 @@ daso_status daso_k_merge(float* x, size_t n, const void* slot, size_t slot_strid
 
 daso_status daso_k_average(float* x, size_t n, const void* slot, size_t slot_stride, int P, int wire, uint32_t* flag,
                            void* stream) {
+    if (n == 0) return DASO_OK;
     if (!x || !aligned16(x)) return DASO_ERR_ARGUMENT;
     if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
     if (!slot_ok(slot, slot_stride, P, wire) || slot_stride < n) return DASO_ERR_ARGUMENT;
@@ -856,6 +860,7 @@ daso_status daso_k_average(float* x, size_t n, const void* slot, size_t slot_str
 }
 
 daso_status daso_k_pack(const float* x, size_t n, void* pack_out, int wire, void* stream) {
+    if (n == 0) return DASO_OK;
     if (!x || !pack_out || !aligned16(x) || !aligned16(pack_out)) return DASO_ERR_ARGUMENT;
     if (wire != DASO_WIRE_BF16 && wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
     daso::KernelArgs a;

@@ -269,3 +269,51 @@ def test_tma_path_bit_identical_to_register_path(n, ops, wire):
     if p1 is not None:
         assert torch.equal(p1[:n].view(torch.int16 if wire == "bf16" else torch.int32),
                            p2[:n].view(torch.int16 if wire == "bf16" else torch.int32))
+
+
+def test_empty_inputs_are_noops():
+    e = torch.empty(0, device="cuda")
+    eb = torch.empty(0, 0, dtype=torch.bfloat16, device="cuda")
+    daso.daso_k_update(e, e, e, 0.1, 0.9, 1e-4, 1.0)
+    daso.daso_k_update(e, e, e, 0.1, 0.9, 1e-4, 1.0, pack_out=torch.empty(0, dtype=torch.bfloat16, device="cuda"))
+    daso.daso_k_merge(e, eb, 1)
+    daso.daso_k_average(e, eb)
+    daso.daso_k_pack(e, torch.empty(0, dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    c = daso.daso_init(1, 1, 4, 1, rank=0, uid=daso.daso_get_unique_id())
+    with pytest.raises(daso.DasoError):
+        c.bind(torch.zeros(8, device="cuda"), torch.zeros(8, device="cuda"), torch.zeros(8, device="cuda"), 0)
+    c.finalize()
+
+
+@pytest.mark.parametrize("impl", ["ldg", "tma"])
+def test_beyond_2_pow_31_elements(impl):
+    """Maximum-size indexing: n = 2^31 + 9 parameters (3 x 8.6 GB buckets), merge with
+    P = 2 bf16 rows of stride > 2^31; sampled elements on both sides of the 2^31
+    boundary and in the ragged tail against the oracle."""
+    n = 2 ** 31 + 9
+    stride = (n + 63) // 64 * 64
+    free, _ = torch.cuda.mem_get_info()
+    if free < 3 * 4 * n + 2 * 2 * stride + (4 << 30):
+        pytest.skip("not enough device memory")
+    prev = daso.daso_kernel_impl(impl)
+    try:
+        X = torch.full((n,), 0.5, device="cuda")
+        V = torch.full((n,), 0.25, device="cuda")
+        Gd = torch.full((n,), 0.125, device="cuda")
+        idx = torch.tensor([0, 1, 2 ** 31 - 1, 2 ** 31, 2 ** 31 + 1, n - 9, n - 2, n - 1], device="cuda")
+        X[idx] = torch.tensor([1.0, -2.0, 3.0, -4.0, 5.0, -6.0, 7.0, -8.0], device="cuda")
+        Gd[idx] = torch.tensor([0.5, 0.25, -1.0, 2.0, -0.5, 1.5, -2.5, 0.75], device="cuda")
+        slot = torch.empty(2, stride, dtype=torch.bfloat16, device="cuda")
+        slot[0].fill_(1.0)
+        slot[1].fill_(-1.0)
+        x, v, g = (t[idx].cpu().numpy() for t in (X, V, Gd))
+        daso.daso_k_update_merge(X, V, Gd, 0.1, 0.9, 1e-4, 0.5, slot, 1, wire="bf16")
+        xu, vo = sgd.sgd_step(x, v, g.astype(np.float64) * 0.5, 0.1, 0.9, 1e-4)
+        xo = numerics.weighted_stale_average(xu, [np.ones(len(x)), -np.ones(len(x))], 1)
+        close(X[idx].cpu().numpy(), xo)
+        close(V[idx].cpu().numpy(), vo)
+    finally:
+        daso.daso_kernel_impl(prev)
+        del X, V, Gd, slot
+        torch.cuda.empty_cache()
