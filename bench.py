@@ -197,6 +197,16 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -290,6 +300,7 @@ def run_ours(a):
     tr = ctx.trace_read(reset=True)
     ctx.trace_enable(False)
     finite = ctx.check_finite()
+    launches_total = int(sum_over_ranks(float(tr["kernel_launches"]), world))
 
     ms_per_step = t_ms / a.steps
     value = 4.0 * n * world / (ms_per_step * 1e-3) / 1e9
@@ -361,7 +372,8 @@ def run_ours(a):
                              "gradient refresh); the inputs (x, v, g = 307 MB) also exceed the 126 MB L2",
                        "value_def": "4 B x n params x N GPUs / ms_per_step", "step_kinds": kinds,
                        "compute_ms_between_steps": a.compute_ms},
-            "roofline": roofline, "phases": phases, "gpu_launches": tr["kernel_launches"],
+            "roofline": roofline, "phases": phases, "gpu_launches": launches_total,
+            "gpu_launches_per_rank": tr["kernel_launches"],
             "clocks": clk.summary(), "e2e": e2e, "finite": finite}
     if world == 1 and not a.no_cpu:
         line["cpu_baseline"] = cpu_baseline(P, G, a.B, a.S, n, a.wire)
