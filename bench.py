@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--S", type=int, default=1)
     ap.add_argument("--n", type=int, default=N_PARAMS)
     ap.add_argument("--topology", default="", help="PxG, default by --gpus")
-    ap.add_argument("--mode", choices=["faithful", "sharded", "fused"], default="fused")
+    ap.add_argument("--mode", choices=["faithful", "sharded", "fused", "nvls"], default="fused")
     ap.add_argument("--wire", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -261,14 +261,18 @@ def run_ours(a):
                          steps_per_epoch=a.B * (1 << 20), momentum=0.9, weight_decay=1e-4, wire=a.wire,
                          mode=a.mode)
     n_pad = daso.daso_padded_numel(n, G)
-    x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+    if a.mode == "nvls":
+        x, g, v = ctx.alloc_bind(n)            # library-owned NCCL symmetric buckets
+    else:
+        x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+        g = torch.zeros_like(x)
+        v = torch.zeros_like(x)
     x[:n] = torch.from_numpy(synthetic.microbench_x0(n)).to(dev)
-    g = torch.zeros_like(x)
-    v = torch.zeros_like(x)
     g_src = torch.zeros_like(x)
     l2_flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     g_src[:n] = torch.from_numpy(synthetic.microbench_grad(n, rank, 0)).to(dev)
-    ctx.bind(x, g, v, n)
+    if a.mode != "nvls":
+        ctx.bind(x, g, v, n)
     stream = torch.cuda.current_stream()
 
     compute = make_compute(a.compute_ms, dev)
@@ -316,16 +320,20 @@ def run_ours(a):
     if traffic is not None:
         roofline["traffic"] = traffic
         roofline["traffic_source"] = tsrc
-    if a.mode == "fused" and G > 1:
+    if a.mode in ("fused", "nvls") and G > 1:
         # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
         # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)
         nvl_bytes = 2.0 * (G - 1) * 4.0 * daso.daso_padded_numel(n, G) / G
+        if a.mode == "nvls":   # switch reads every element of this GPU's g + multicast store of the shard
+            nvl_bytes = 4.0 * daso.daso_padded_numel(n, G) * (1.0 + 1.0 / G)
         nvl_gbs = nvl_bytes / (tr["kernel_ms"] / max(tr["kernel_launches"], 1) * 1e-3) / 1e9
         nvl_gbs = -max_over_ranks(-nvl_gbs, world)
         roofline = {"bound": "nvlink", "achieved": nvl_gbs, "peak": 770.0, "unit": "GB/s",
                     "frac": nvl_gbs / 770.0, "traffic": None,
-                    "kernel": "peer_kernel (node gradient reduce over NVLink + update [+merge] [+pack] + "
-                              "parameter all-gather by NVLink stores)",
+                    "kernel": ("nvls_kernel (node gradient reduce in the NVSwitch by multimem.ld_reduce + update "
+                               "[+merge] [+pack] + parameter broadcast by multimem.st)") if a.mode == "nvls" else
+                              ("peer_kernel (node gradient reduce over NVLink + update [+merge] [+pack] + "
+                               "parameter all-gather by NVLink stores)"),
                     "bytes_per_launch": nvl_bytes, "bytes_def": "NVLink bytes per direction per GPU",
                     "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1),
                     "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)",

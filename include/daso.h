@@ -48,10 +48,13 @@ enum { DASO_WIRE_BF16 = 0, DASO_WIRE_FP32 = 1 };                 /* P:86 / P:88,
 enum { DASO_MODE_FAITHFUL = 0,  /* v1: rotating group exchange + node broadcast (Fig. 4)   */
        DASO_MODE_SHARDED = 1,   /* v2: node reduce-scatter, shard update, all groups exchange
                                    their shard, node all-gather; numerically the same */
-       DASO_MODE_FUSED = 2 };   /* v3: the sharded batch with the node tier (gradient reduce over
+       DASO_MODE_FUSED = 2,     /* v3: the sharded batch with the node tier (gradient reduce over
                                    peers + update/merge/pack + parameter all-gather) in ONE kernel
                                    over NVLink peer memory (CUDA IPC); G <= 8; caller buffers must
                                    be cudaMalloc-backed (torch's default allocator is) */
+       DASO_MODE_NVLS = 3 };    /* v4: as FUSED, but the gradient reduce runs inside the NVSwitch
+                                   (multimem.ld_reduce) and the parameter shard is broadcast by one
+                                   multimem.st; buckets must come from daso_alloc_bind */
 
 const char* daso_status_string(daso_status s);
 const char* daso_version(void);
@@ -165,6 +168,14 @@ size_t daso_padded_numel(size_t n, int gpus_per_node);
  * allocates its ring of exchange slots here: [P][n_pad] wire elements (n_pad = n
  * rounded up to 64 * G).  Errors: DASO_ERR_PROTOCOL (bound twice), DASO_ERR_ARGUMENT. */
 daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n);
+
+/* Allocate the flat buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed) in
+ * library-owned memory and bind them; returns the device pointers (owned by the library,
+ * valid until daso_finalize).  x and g are NCCL symmetric memory (ncclMemAlloc) registered
+ * as windows on the node communicator, which DASO_MODE_NVLS requires for its multicast
+ * addresses; collective over the node.  Errors: as daso_bind; DASO_ERR_CONFIG if the node
+ * has no NVLS multicast support (NVLS mode). */
+daso_status daso_alloc_bind(daso_ctx* c, size_t n, float** x, float** g, float** v);
 
 /* ----- split API (each a collective over the world; what daso_step composes) -----
  * daso_local_sync: g <- sum of g over the node (in place, NCCL all-reduce over

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libdaso.so")
 OK, ERR_CONFIG, ERR_RANGE, ERR_PROTOCOL, ERR_ARGUMENT, ERR_CUDA, ERR_NCCL, ERR_NONFINITE = range(8)
 WARMUP, CYCLING, COOLDOWN = 0, 1, 2
 WIRE_BF16, WIRE_FP32 = 0, 1
-MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED = 0, 1, 2
+MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED, MODE_NVLS = 0, 1, 2, 3
 STEP_GRADS_REDUCED = 1
 
 
@@ -82,6 +82,8 @@ _SIG = {
     "daso_init": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Config),
                             C.c_void_p]),
     "daso_bind": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]),
+    "daso_alloc_bind": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_void_p)]),
     "daso_local_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "daso_local_update": (C.c_int, [C.c_void_p, C.c_float, C.c_void_p]),
     "daso_global_send": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),

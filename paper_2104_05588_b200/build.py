@@ -61,7 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = common + ["-x", "cu", "-c", src, "-o", obj]
+        lang = "c++" if src.endswith(".cpp") else "cu"   # .cpp: host-only C++ (no device code)
+        cmd = common + ["-x", lang, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), file=sys.stderr)

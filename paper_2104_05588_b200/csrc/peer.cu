@@ -371,7 +371,151 @@ int dispatch_peer(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
     }
 }
 
+
+// ---- NVLS variant (DASO_MODE_NVLS; SURVEY §8(f) N1 as specified): the node gradient
+// reduce is done inside the NVSwitch — multimem.ld_reduce on the multicast address of g
+// returns the sum over the node's G GPUs of this shard — and the new parameter shard is
+// written to every GPU of the node by ONE multimem.st through the switch.  Per GPU and
+// direction 4n(1 + 1/G) bytes cross NVLink instead of 8n(G-1)/G (fewer for G >= 4).
+// The switch's summation order is fixed by the hardware, not ascending local id (R18);
+// each element's sum is formed once, so node replicas stay bitwise identical.
+__device__ __forceinline__ float4 mm_ld_reduce_add(const float* p) {
+    float4 r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ float mm_ld_reduce_add1(const float* p) {
+    float r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void mm_st(float* p, float4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void mm_st1(float* p, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+template <int OPS, int WIRE, int N>
+__device__ __forceinline__ void nvls_body(const PeerArgs& pa, int64_t i, bool& bad) {
+    const KernelArgs& a = pa.a;
+    float x[N], v[N], g[N];
+    if constexpr (N == 8) {
+        const float4 g0 = mm_ld_reduce_add(pa.g_mc + i), g1 = mm_ld_reduce_add(pa.g_mc + i + 4);
+        g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) g[j] = mm_ld_reduce_add1(pa.g_mc + i + j);
+    }
+    ld_f32<N>(a.x + i, x);
+    ld_f32<N>(a.v + i, v);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
+        v[j] = fmaf(a.mu, v[j], d);
+        x[j] = fmaf(-a.lr, v[j], x[j]);
+    }
+    st_f32<N>(a.v + i, v);
+    if constexpr ((OPS & OP_MERGE) != 0) {
+        float acc[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[j] = 0.f;
+#pragma unroll 4
+        for (int p = 0; p < a.P; ++p) {
+            float s[N];
+            Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[j] += s[j] - x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;
+    }
+    if constexpr (N == 8) {
+        mm_st(pa.x_mc + i, make_float4(x[0], x[1], x[2], x[3]));
+        mm_st(pa.x_mc + i + 4, make_float4(x[4], x[5], x[6], x[7]));
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) mm_st1(pa.x_mc + i + j, x[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
+    if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
+}
+
+template <int OPS, int WIRE>
+__global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
+    const int G = pa.G;
+    if (blockIdx.x == 0 && threadIdx.x < G) {   // 1. start barrier: every peer's g is complete
+        __threadfence_system();
+        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
+    }
+    if (threadIdx.x == 0)
+        for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + q, pa.epoch, pa.err);
+    __syncthreads();
+    bool bad = false;
+    const int64_t n = pa.a.n;
+    const int64_t nch = n / 8;
+    const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
+    for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
+        nvls_body<OPS, WIRE, 8>(pa, c * 8, bad);
+    if (blockIdx.x == gridDim.x - 1) {
+        const int64_t i = nch * 8 + threadIdx.x;
+        if (i < n) nvls_body<OPS, WIRE, 1>(pa, i, bad);
+    }
+    if (pa.a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
+    }
+    __syncthreads();                             // 3. end barrier: every peer's shard has landed
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(pa.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
+            __threadfence_system();
+            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
+            for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + G + q, pa.epoch, pa.err);
+        }
+    }
+}
+
+template <int OPS, int WIRE>
+int launch_nvls_t(const PeerArgs& pa, cudaStream_t s, int sms) {
+    const int64_t nch = pa.a.n / 8;
+    int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
+    nvls_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
+    return int(cudaGetLastError());
+}
+
+template <int WIRE>
+int dispatch_nvls(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
+    switch (ops) {
+        case OP_UPDATE: return launch_nvls_t<OP_UPDATE, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_PACK: return launch_nvls_t<OP_UPDATE | OP_PACK, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_MERGE: return launch_nvls_t<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_MERGE | OP_PACK: return launch_nvls_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
+
 }  // namespace
+
+int launch_nvls(int ops, int wire, const PeerArgs& pa, void* stream) {
+    if (pa.G < 1 || pa.G > kMaxPeers || !pa.x_mc || !pa.g_mc) return int(cudaErrorInvalidValue);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (wire == DASO_WIRE_BF16) return dispatch_nvls<DASO_WIRE_BF16>(ops, pa, s, sms);
+    if (wire == DASO_WIRE_FP32) return dispatch_nvls<DASO_WIRE_FP32>(ops, pa, s, sms);
+    return int(cudaErrorInvalidValue);
+}
 
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream) {
     if (pa.G < 1 || pa.G > kMaxPeers) return int(cudaErrorInvalidValue);

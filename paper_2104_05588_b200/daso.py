@@ -15,7 +15,7 @@ from . import _lib as L
 from ._lib import DasoError, Record, check, lib  # noqa: F401
 
 WIRES = {"bf16": L.WIRE_BF16, "fp32": L.WIRE_FP32}
-MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED}
+MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED, "nvls": L.MODE_NVLS}
 
 
 def _torch():
@@ -139,6 +139,23 @@ class Ctx:
         self._keep = (x, g, v)
         self.n = n
         self._check(lib().daso_bind(self._h, _ptr(x), _ptr(g), _ptr(v), n), "daso_bind")
+
+    def alloc_bind(self, n: int):
+        """daso_alloc_bind: library-owned buckets (required by the "nvls" mode); returns torch
+        tensors x, g, v of daso_padded_numel(n, G) floats viewing them (valid until finalize)."""
+        torch = _torch()
+        px, pg, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self._check(lib().daso_alloc_bind(self._h, int(n), C.byref(px), C.byref(pg), C.byref(pv)), "daso_alloc_bind")
+        self.n = int(n)
+        n_pad = daso_padded_numel(n, self.G)
+
+        class _Buf:
+            def __init__(self, ptr, owner):
+                self._owner = owner
+                self.__cuda_array_interface__ = {"shape": (n_pad,), "typestr": "<f4", "data": (int(ptr), False),
+                                                 "version": 3, "strides": None}
+        dev = torch.device("cuda", torch.cuda.current_device())
+        return tuple(torch.as_tensor(_Buf(p.value, self), device=dev) for p in (px, pg, pv))
 
     def local_sync(self, stream=None):
         self._check(lib().daso_local_sync(self._h, _stream(stream)), "daso_local_sync")
@@ -406,7 +423,9 @@ class FlatParams:
     "buffer packaging") and re-point every parameter and its ``.grad`` as views,
     so the per-step unpack is free.  Buckets x, g, v hold n_pad elements."""
 
-    def __init__(self, params, gpus_per_node: int = 1, align: int = 64):
+    def __init__(self, params, gpus_per_node: int = 1, align: int = 64, ctx: "Ctx | None" = None):
+        """ctx given: the buckets are allocated and bound by the library (daso_alloc_bind —
+        required for the "nvls" mode); otherwise torch allocates them and the caller binds."""
         torch = _torch()
         self.params = [p for p in params if p.requires_grad]
         if not self.params:
@@ -414,9 +433,12 @@ class FlatParams:
         dev = self.params[0].device
         self.offsets, self.n = daso_flat_layout([p.numel() for p in self.params], align)
         self.n_pad = daso_padded_numel(self.n, gpus_per_node)
-        self.x = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
-        self.g = torch.zeros_like(self.x)
-        self.v = torch.zeros_like(self.x)
+        if ctx is not None:
+            self.x, self.g, self.v = ctx.alloc_bind(self.n)
+        else:
+            self.x = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
+            self.g = torch.zeros_like(self.x)
+            self.v = torch.zeros_like(self.x)
         daso_k_gather([p.detach() for p in self.params], self.x, self.offsets)
         torch.cuda.current_stream().synchronize()
         # views keep each parameter's memory format (e.g. channels_last): the bucket holds

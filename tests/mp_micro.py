@@ -41,11 +41,14 @@ def main():
     ctx = daso.daso_init(world, a.G, 4, 1, rank=rank, uid=uid, total_epochs=1, steps_per_epoch=4 << 20,
                          momentum=0.9, weight_decay=1e-4, wire=a.wire, mode=a.mode)
     n_pad = daso.daso_padded_numel(N, a.G)
-    x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+    if a.mode == "nvls":
+        x, g, v = ctx.alloc_bind(N)
+    else:
+        x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+        g = torch.zeros_like(x)
+        v = torch.zeros_like(x)
+        ctx.bind(x, g, v, N)
     x[:N] = torch.from_numpy(synthetic.microbench_x0(N)).to(dev)
-    g = torch.zeros_like(x)
-    v = torch.zeros_like(x)
-    ctx.bind(x, g, v, N)
     idx = torch.from_numpy(sample_indices()).to(dev)
     trace = []
     for k in range(a.steps):

@@ -62,10 +62,13 @@ def run_toy(a, rank: int = 0, world: int = 1, uid: bytes | None = None):
                          cooldown_epochs=a.cooldown, total_epochs=a.epochs, steps_per_epoch=a.spe,
                          momentum=a.mu, weight_decay=a.wd, wire=a.wire, mode=a.mode)
     n_pad = daso.daso_padded_numel(a.d, a.G)
-    x = torch.zeros(n_pad, dtype=torch.float32, device=dev)      # x0 = 0, identical on every rank (R17)
-    g = torch.zeros_like(x)
-    v = torch.zeros_like(x)
-    ctx.bind(x, g, v, a.d)
+    if a.mode == "nvls":                                          # library-owned symmetric buckets
+        x, g, v = ctx.alloc_bind(a.d)                             # zeroed: x0 = 0 on every rank (R17)
+    else:
+        x = torch.zeros(n_pad, dtype=torch.float32, device=dev)  # x0 = 0, identical on every rank (R17)
+        g = torch.zeros_like(x)
+        v = torch.zeros_like(x)
+        ctx.bind(x, g, v, a.d)
     sched = Schedule(a.B, a.S, a.warmup, a.cooldown, a.epochs, a.spe, a.G) if a.split else None
     trace, recs, cks = [], [], []
     ck = torch.zeros(1, dtype=torch.int64, device=dev)
