@@ -405,46 +405,95 @@ template <int OPS, int WIRE, int N>
 __device__ __forceinline__ void nvls_body(const PeerArgs& pa, int64_t i, bool& bad) {
     const KernelArgs& a = pa.a;
     float x[N], v[N], g[N];
-    if constexpr (N == 8) {
-        const float4 g0 = mm_ld_reduce_add(pa.g_mc + i), g1 = mm_ld_reduce_add(pa.g_mc + i + 4);
-        g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+    if constexpr (N % 4 == 0) {
+        float4 gv[N / 4];
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q) gv[q] = mm_ld_reduce_add(pa.g_mc + i + 4 * q);   // all in flight
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q) {
+            g[4 * q] = gv[q].x; g[4 * q + 1] = gv[q].y; g[4 * q + 2] = gv[q].z; g[4 * q + 3] = gv[q].w;
+        }
+#pragma unroll
+        for (int q = 0; q < N / 8; ++q) {
+            float xt[8], vt[8];
+            ld_f32<8>(a.x + i + 8 * q, xt);
+            ld_f32<8>(a.v + i + 8 * q, vt);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { x[8 * q + j] = xt[j]; v[8 * q + j] = vt[j]; }
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) g[j] = mm_ld_reduce_add1(pa.g_mc + i + j);
+        ld_f32<N>(a.x + i, x);
+        ld_f32<N>(a.v + i, v);
     }
-    ld_f32<N>(a.x + i, x);
-    ld_f32<N>(a.v + i, v);
 #pragma unroll
     for (int j = 0; j < N; ++j) {
         const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
         v[j] = fmaf(a.mu, v[j], d);
         x[j] = fmaf(-a.lr, v[j], x[j]);
     }
-    st_f32<N>(a.v + i, v);
+    if constexpr (N % 8 == 0) {
+#pragma unroll
+        for (int q = 0; q < N / 8; ++q) {
+            float vt[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) vt[j] = v[8 * q + j];
+            st_f32<8>(a.v + i + 8 * q, vt);
+        }
+    } else {
+        st_f32<N>(a.v + i, v);
+    }
     if constexpr ((OPS & OP_MERGE) != 0) {
         float acc[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[j] = 0.f;
-#pragma unroll 4
+#pragma unroll 2
         for (int p = 0; p < a.P; ++p) {
-            float s[N];
-            Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
 #pragma unroll
-            for (int j = 0; j < N; ++j) acc[j] += s[j] - x[j];
+            for (int q = 0; q < (N + 7) / 8; ++q) {
+                constexpr int M = N < 8 ? N : 8;
+                float s[M];
+                Wire<WIRE>::template load<M>(a.slot, p * a.slot_stride + i + 8 * q, s);
+#pragma unroll
+                for (int j = 0; j < M; ++j) acc[8 * q + j] += s[j] - x[8 * q + j];
+            }
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;
     }
-    if constexpr (N == 8) {
-        mm_st(pa.x_mc + i, make_float4(x[0], x[1], x[2], x[3]));
-        mm_st(pa.x_mc + i + 4, make_float4(x[4], x[5], x[6], x[7]));
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q)
+            mm_st(pa.x_mc + i + 4 * q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
     } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) mm_st1(pa.x_mc + i + j, x[j]);
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
-    if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
+    if constexpr ((OPS & OP_PACK) != 0) {
+#pragma unroll
+        for (int q = 0; q < (N + 7) / 8; ++q) {
+            constexpr int M = N < 8 ? N : 8;
+            float t[M];
+#pragma unroll
+            for (int j = 0; j < M; ++j) t[j] = x[8 * q + j];
+            Wire<WIRE>::template store<M>(a.pack_out, i + 8 * q, t);
+        }
+    }
+}
+
+constexpr int kNV = 16;   // parameters per thread per iteration: 4 multimem.ld_reduce.v4 in flight
+
+int nvls_blocks_per_sm() {   // DASO_NVLS_BPSM, default 8
+    static int v = 0;
+    if (v == 0) {
+        const char* e = getenv("DASO_NVLS_BPSM");
+        v = e ? atoi(e) : 8;
+        if (v < 1) v = 1;
+    }
+    return v;
 }
 
 template <int OPS, int WIRE>
@@ -459,13 +508,12 @@ __global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
     __syncthreads();
     bool bad = false;
     const int64_t n = pa.a.n;
-    const int64_t nch = n / 8;
+    const int64_t nch = n / kNV;
     const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
     for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
-        nvls_body<OPS, WIRE, 8>(pa, c * 8, bad);
+        nvls_body<OPS, WIRE, kNV>(pa, c * kNV, bad);
     if (blockIdx.x == gridDim.x - 1) {
-        const int64_t i = nch * 8 + threadIdx.x;
-        if (i < n) nvls_body<OPS, WIRE, 1>(pa, i, bad);
+        for (int64_t i = nch * kNV + threadIdx.x; i < n; i += kPeerThreads) nvls_body<OPS, WIRE, 1>(pa, i, bad);
     }
     if (pa.a.flag != nullptr) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
@@ -486,9 +534,9 @@ __global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
 
 template <int OPS, int WIRE>
 int launch_nvls_t(const PeerArgs& pa, cudaStream_t s, int sms) {
-    const int64_t nch = pa.a.n / 8;
+    const int64_t nch = pa.a.n / kNV;
     int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * nvls_blocks_per_sm()));
     nvls_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
     return int(cudaGetLastError());
 }
