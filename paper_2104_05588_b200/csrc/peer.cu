@@ -484,13 +484,16 @@ __device__ __forceinline__ void nvls_body(const PeerArgs& pa, int64_t i, bool& b
     }
 }
 
-constexpr int kNV = 16;   // parameters per thread per iteration: 4 multimem.ld_reduce.v4 in flight
+constexpr int kNV = 8;   // parameters per thread per iteration: 2 multimem.ld_reduce.v4 in flight
 
-int nvls_blocks_per_sm() {   // DASO_NVLS_BPSM, default 8
+// Total CTAs of the NVLS kernel (DASO_NVLS_CTAS).  Unlike the peer kernels, multicast
+// requests congest the switch when too many are in flight: 296 CTAs x 2 reduces ran at 0.43 of
+// the link, 1184 CTAs x 4 at 0.19-0.23 (profiles/r01).
+int nvls_ctas() {
     static int v = 0;
     if (v == 0) {
-        const char* e = getenv("DASO_NVLS_BPSM");
-        v = e ? atoi(e) : 8;
+        const char* e = getenv("DASO_NVLS_CTAS");
+        v = e ? atoi(e) : 64;
         if (v < 1) v = 1;
     }
     return v;
@@ -536,7 +539,8 @@ template <int OPS, int WIRE>
 int launch_nvls_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     const int64_t nch = pa.a.n / kNV;
     int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * nvls_blocks_per_sm()));
+    (void)sms;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, nvls_ctas()));
     nvls_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
     return int(cudaGetLastError());
 }
