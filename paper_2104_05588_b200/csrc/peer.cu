@@ -486,14 +486,15 @@ __device__ __forceinline__ void nvls_body(const PeerArgs& pa, int64_t i, bool& b
 
 constexpr int kNV = 8;   // parameters per thread per iteration: 2 multimem.ld_reduce.v4 in flight
 
-// Total CTAs of the NVLS kernel (DASO_NVLS_CTAS).  Unlike the peer kernels, multicast
-// requests congest the switch when too many are in flight: 296 CTAs x 2 reduces ran at 0.43 of
-// the link, 1184 CTAs x 4 at 0.19-0.23 (profiles/r01).
+// Total CTAs of the NVLS kernel (DASO_NVLS_CTAS, default 296 = 2 per SM).  Measured at 1x4
+// (profiles/r01/b17_*, b18_*): 32..296 CTAs x 2 reduces in flight all run at ~0.43 of the link,
+// 16 CTAs at 0.29, 1184 CTAs x 4 reduces at 0.19-0.23 — the multicast path saturates well below
+// the P2P TMA kernel (0.79) on this box.
 int nvls_ctas() {
     static int v = 0;
     if (v == 0) {
         const char* e = getenv("DASO_NVLS_CTAS");
-        v = e ? atoi(e) : 64;
+        v = e ? atoi(e) : 296;
         if (v < 1) v = 1;
     }
     return v;
