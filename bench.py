@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--nccl-max-ctas", type=int, default=0, help="cap the side-stream exchange's NCCL CTAs")
     ap.add_argument("--compute-ms", type=float, default=0.0,
                     help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
                          "the global exchange the next batch's compute hides")
@@ -259,7 +260,7 @@ def run_ours(a):
     uid = daso.rendezvous_unique_id() if world > 1 else daso.daso_get_unique_id()
     ctx = daso.daso_init(world, G, a.B, a.S, rank=rank, uid=uid, total_epochs=1,
                          steps_per_epoch=a.B * (1 << 20), momentum=0.9, weight_decay=1e-4, wire=a.wire,
-                         mode=a.mode)
+                         mode=a.mode, nccl_max_ctas=a.nccl_max_ctas)
     n_pad = daso.daso_padded_numel(n, G)
     if a.mode == "nvls":
         x, g, v = ctx.alloc_bind(n)            # library-owned NCCL symmetric buckets

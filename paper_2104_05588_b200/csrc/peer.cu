@@ -332,7 +332,13 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
         attr = true;
     }
     const size_t smem = size_t(NS) * L.in_bytes + size_t(kPeerOut) * L.out_bytes + 8 * size_t(NS);
-    peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(sms)), dim3(kPeerThreads), smem, s>>>(pa, NS);
+    static int ctas = -1;   // DASO_PEER_TMA_CTAS: persistent CTAs (default: one per SM)
+    if (ctas < 0) {
+        const char* e = getenv("DASO_PEER_TMA_CTAS");
+        ctas = e ? std::max(1, atoi(e)) : 0;
+    }
+    const int grid = ctas > 0 ? std::min(ctas, sms) : sms;
+    peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
 }
 
