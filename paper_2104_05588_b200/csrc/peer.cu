@@ -332,12 +332,15 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
         attr = true;
     }
     const size_t smem = size_t(NS) * L.in_bytes + size_t(kPeerOut) * L.out_bytes + 8 * size_t(NS);
-    static int ctas = -1;   // DASO_PEER_TMA_CTAS: persistent CTAs (default: one per SM)
+    // DASO_PEER_TMA_CTAS: persistent CTAs.  Default: one per SM minus 16, so the side-stream
+    // exchange's NCCL kernels always find free SMs (2x2: exchange hidden 0.98 vs 0.73 with every
+    // SM taken, same kernel time; profiles/r01/b20_*).
+    static int ctas = -1;
     if (ctas < 0) {
         const char* e = getenv("DASO_PEER_TMA_CTAS");
         ctas = e ? std::max(1, atoi(e)) : 0;
     }
-    const int grid = ctas > 0 ? std::min(ctas, sms) : sms;
+    const int grid = ctas > 0 ? std::min(ctas, sms) : std::max(1, sms - 16);
     peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
 }
