@@ -354,6 +354,30 @@ def daso_k_checksum(x, out_u64, stream=None):
 
 
 # ------------------------------------------------------------------ backward-overlapped local sync
+def bucket_partition(offsets, numels, n, limit):
+    """Split the flat gradient bucket into contiguous all-reduce buckets in reverse parameter
+    order (the order backward produces gradients), each >= `limit` elements except the last.
+    Returns (buckets: lists of parameter indices, ranges: (offset, count) per bucket); the
+    ranges tile [0, offset_last + numel_last) exactly, inter-parameter padding included."""
+    m = len(offsets)
+    buckets, cur = [], []
+    for i in range(m - 1, -1, -1):
+        cur.append(i)
+        lo = offsets[cur[-1]]
+        hi = offsets[cur[0]] + numels[cur[0]]
+        if hi - lo >= limit:
+            buckets.append(cur)
+            cur = []
+    if cur:
+        buckets.append(cur)
+    ranges = []
+    for b in buckets:
+        lo = offsets[b[-1]]
+        hi = offsets[b[0] + 1] if b[0] + 1 < m else offsets[b[0]] + numels[b[0]]
+        ranges.append((lo, min(hi, n) - lo))
+    return buckets, ranges
+
+
 class OverlappedLocalSync:
     """Bucketed node all-reduce overlapped with backward (the DDP
     behaviour of the paper's local tier).  Buckets are contiguous ranges of the
@@ -366,23 +390,8 @@ class OverlappedLocalSync:
         torch = _torch()
         self.ctx, self.flat = ctx, flat
         self.stream = torch.cuda.Stream(priority=-1)
-        limit = int(bucket_mb * (1 << 20) / 4)
-        order = list(range(len(flat.params)))[::-1]            # backward produces grads ~ in reverse
-        self.buckets, cur = [], []
-        for i in order:
-            cur.append(i)
-            lo = flat.offsets[cur[-1]]
-            hi = flat.offsets[cur[0]] + flat.params[cur[0]].numel()
-            if hi - lo >= limit:
-                self.buckets.append(cur)
-                cur = []
-        if cur:
-            self.buckets.append(cur)
-        self.ranges = []
-        for b in self.buckets:
-            lo = flat.offsets[b[-1]]
-            hi = flat.offsets[b[0]] + flat.params[b[0]].numel() if b[0] == len(flat.params) - 1 else flat.offsets[b[0] + 1]
-            self.ranges.append((lo, min(hi, flat.n) - lo))
+        self.buckets, self.ranges = bucket_partition(flat.offsets, [p.numel() for p in flat.params], flat.n,
+                                                     int(bucket_mb * (1 << 20) / 4))
         self.bucket_of = {i: k for k, b in enumerate(self.buckets) for i in b}
         self.pending = [len(b) for b in self.buckets]
         self.launched = 0

@@ -116,3 +116,26 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(L, "_lib", None)
     with pytest.raises(ImportError):
         L.lib()
+
+
+def test_bucket_partition_tiles_the_bucket():
+    """OverlappedLocalSync's buckets (N2) cover every gradient exactly once, contiguously,
+    in backward order."""
+    import random
+    from paper_2104_05588_b200.daso import bucket_partition
+    rnd = random.Random(0)
+    for trial in range(200):
+        numels = [rnd.randint(1, 5000) for _ in range(rnd.randint(1, 40))]
+        offsets, n = daso.daso_flat_layout(numels, 64)
+        limit = rnd.randint(1, 20000)
+        buckets, ranges = bucket_partition(offsets, numels, n, limit)
+        assert sorted(i for b in buckets for i in b) == list(range(len(numels)))
+        assert [i for b in buckets for i in b] == list(range(len(numels) - 1, -1, -1))
+        end = offsets[-1] + numels[-1]
+        pos = end
+        for (off, cnt), b in zip(ranges, buckets):          # descending, adjacent ranges
+            assert off + cnt == pos and cnt > 0
+            pos = off
+            assert all(offsets[i] >= off and offsets[i] + numels[i] <= off + cnt for i in b)
+        assert pos == 0
+        assert all(cnt >= limit for (_, cnt) in ranges[:-1]) or len(ranges) == 1
