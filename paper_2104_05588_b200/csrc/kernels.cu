@@ -79,13 +79,11 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
     if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
 }
 
-// Parameters per thread: 8 for the update kernels (>= 3 fp32 streams: 6+ 128-bit loads in
-// flight per thread already); 32 for the light kernels (average, pack: 1-2 streams), whose
-// 8-wide version left DRAM at 48-68 % under ncu; 16 for merge-only (register pressure).
+// Parameters per thread: 8 for every op set.  Widening the light kernels (average, pack) to
+// 32 per thread (4x fewer CTAs, more loads in flight per thread) made them slower on B200:
+// K4 41 -> 57 us, pack 23 -> 37 us (profiles/r01/kernel_bench_wide_light.json).
 template <int OPS>
-__host__ __device__ constexpr int vec_of() {
-    return (OPS & OP_UPDATE) ? kVec : (OPS & OP_MERGE) ? 2 * kVec : 4 * kVec;
-}
+__host__ __device__ constexpr int vec_of() { return kVec; }
 
 template <int OPS, int WIRE>
 __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
