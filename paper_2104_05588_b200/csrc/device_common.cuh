@@ -17,14 +17,11 @@ constexpr int kVec = 8;
 // ----------------------------------------------------------------- fp32 streams
 template <int N>
 __device__ __forceinline__ void ld_f32(const float* p, float (&r)[N]) {
-    if constexpr (N % 4 == 0) {
-        float4 q[N / 4];
-#pragma unroll
-        for (int k = 0; k < N / 4; ++k) q[k] = __ldcs(reinterpret_cast<const float4*>(p) + k);   // all in flight
-#pragma unroll
-        for (int k = 0; k < N / 4; ++k) {
-            r[4 * k] = q[k].x; r[4 * k + 1] = q[k].y; r[4 * k + 2] = q[k].z; r[4 * k + 3] = q[k].w;
-        }
+    if constexpr (N == 8) {
+        float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+        float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+        r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+        r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
     } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) r[j] = __ldcs(p + j);
@@ -33,10 +30,9 @@ __device__ __forceinline__ void ld_f32(const float* p, float (&r)[N]) {
 
 template <int N>
 __device__ __forceinline__ void st_f32(float* p, const float (&r)[N]) {
-    if constexpr (N % 4 == 0) {
-#pragma unroll
-        for (int k = 0; k < N / 4; ++k)
-            __stcs(reinterpret_cast<float4*>(p) + k, make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+    if constexpr (N == 8) {
+        __stcs(reinterpret_cast<float4*>(p), make_float4(r[0], r[1], r[2], r[3]));
+        __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(r[4], r[5], r[6], r[7]));
     } else {
 #pragma unroll
         for (int j = 0; j < N; ++j) __stcs(p + j, r[j]);
@@ -59,17 +55,10 @@ struct Wire<DASO_WIRE_BF16> {
     template <int N>
     static __device__ __forceinline__ void load(const void* base, int64_t i, float (&r)[N]) {
         const uint16_t* p = static_cast<const uint16_t*>(base) + i;
-        if constexpr (N % 8 == 0) {
-            uint4 q[N / 8];
-#pragma unroll
-            for (int k = 0; k < N / 8; ++k) q[k] = __ldcs(reinterpret_cast<const uint4*>(p) + k);
-#pragma unroll
-            for (int k = 0; k < N / 8; ++k) {
-                const uint4 u = q[k];
-                float* o = r + 8 * k;
-                o[0] = bf16lo(u.x); o[1] = bf16hi(u.x); o[2] = bf16lo(u.y); o[3] = bf16hi(u.y);
-                o[4] = bf16lo(u.z); o[5] = bf16hi(u.z); o[6] = bf16lo(u.w); o[7] = bf16hi(u.w);
-            }
+        if constexpr (N == 8) {
+            uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+            r[0] = bf16lo(u.x); r[1] = bf16hi(u.x); r[2] = bf16lo(u.y); r[3] = bf16hi(u.y);
+            r[4] = bf16lo(u.z); r[5] = bf16hi(u.z); r[6] = bf16lo(u.w); r[7] = bf16hi(u.w);
         } else {
 #pragma unroll
             for (int j = 0; j < N; ++j) r[j] = __uint_as_float(uint32_t(p[j]) << 16);
@@ -78,14 +67,10 @@ struct Wire<DASO_WIRE_BF16> {
     template <int N>
     static __device__ __forceinline__ void store(void* base, int64_t i, const float (&r)[N]) {
         uint16_t* p = static_cast<uint16_t*>(base) + i;
-        if constexpr (N % 8 == 0) {
-#pragma unroll
-            for (int k = 0; k < N / 8; ++k) {
-                const float* q = r + 8 * k;
-                __stcs(reinterpret_cast<uint4*>(p) + k,
-                       make_uint4(pack_bf16x2(q[0], q[1]), pack_bf16x2(q[2], q[3]), pack_bf16x2(q[4], q[5]),
-                                  pack_bf16x2(q[6], q[7])));
-            }
+        if constexpr (N == 8) {
+            uint4 u = make_uint4(pack_bf16x2(r[0], r[1]), pack_bf16x2(r[2], r[3]),
+                                 pack_bf16x2(r[4], r[5]), pack_bf16x2(r[6], r[7]));
+            __stcs(reinterpret_cast<uint4*>(p), u);
         } else {
 #pragma unroll
             for (int j = 0; j < N; ++j) p[j] = __bfloat16_as_ushort(__float2bfloat16_rn(r[j]));

@@ -79,22 +79,20 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
     if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
 }
 
-// Parameters per thread: 8 for every op set.  Widening the light kernels (average, pack) to
-// 32 per thread (4x fewer CTAs, more loads in flight per thread) made them slower on B200:
-// K4 41 -> 57 us, pack 23 -> 37 us (profiles/r01/kernel_bench_wide_light.json).
-template <int OPS>
-__host__ __device__ constexpr int vec_of() { return kVec; }
-
+// Eight parameters per thread for every op set.  Measured alternatives (profiles/r01): 32 per
+// thread for the light kernels (average, pack) was slower (K4 41 -> 57 us, pack 23 -> 37 us), and
+// issuing the two 128-bit loads of a stream from an array loop instead of two named loads cost K1
+// 9 % (75 -> 82 us, same box, A/B in one run): ptxas schedules the explicit form better.
 template <int OPS, int WIRE>
 __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
-    constexpr int V = vec_of<OPS>();
-    const int64_t nchunks = a.n / V;
+    const int64_t nchunks = a.n / kVec;
     const int64_t stride = int64_t(gridDim.x) * kThreads;
     bool bad = false;
     for (int64_t c = int64_t(blockIdx.x) * kThreads + threadIdx.x; c < nchunks; c += stride)
-        body<OPS, WIRE, V>(a, c * V, bad);
-    if (blockIdx.x == gridDim.x - 1) {                           // ragged tail (< V elements)
-        for (int64_t i = nchunks * V + threadIdx.x; i < a.n; i += kThreads) body<OPS, WIRE, 1>(a, i, bad);
+        body<OPS, WIRE, kVec>(a, c * kVec, bad);
+    if (blockIdx.x == gridDim.x - 1) {                           // ragged tail (< 8 elements)
+        const int64_t i = nchunks * kVec + threadIdx.x;
+        if (i < a.n) body<OPS, WIRE, 1>(a, i, bad);
     }
     if (a.flag != nullptr) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
@@ -256,7 +254,7 @@ int launch_t(const KernelArgs& a, cudaStream_t s) {
     // One 8-parameter chunk per thread ("one-shot" grid): measured 95% of the copy
     // peak for K1 on B200 vs 82% for a persistent grid-stride grid of SMs x occupancy
     // (tools/k1_variants.cu); the grid-stride loop only engages past 2^31 blocks.
-    const int64_t nchunks = a.n / vec_of<OPS>();
+    const int64_t nchunks = a.n / kVec;
     int64_t blocks = (nchunks + kThreads - 1) / kThreads;
     if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;
     if (blocks < 1) blocks = 1;
