@@ -166,31 +166,12 @@ int launch_peer_t(const PeerArgs& pa, cudaStream_t s, int sms) {
 // NVLink-mapped global addresses) through an mbarrier ring of shared-memory stages, one
 // persistent CTA per SM.  Per tile: own x, v + G gradient tiles (G-1 remote) in; x out
 // to G peers (G-1 remote), v and the packed row out locally.
-
-int peer_tile() {   // DASO_PEER_TILE: parameters per TMA tile (1024, 2048 default, 4096)
-    static int v = 0;
-    if (v == 0) {
-        const char* e = getenv("DASO_PEER_TILE");
-        v = e ? atoi(e) : 2048;
-        if (v != 1024 && v != 4096) v = 2048;
-    }
-    return v;
-}
-
-int peer_ctas_per_sm() {   // DASO_PEER_CTAS_PER_SM: 1 (default, ~210 KB of stages) or 2 (~100 KB each)
-    static int v = 0;
-    if (v == 0) {
-        const char* e = getenv("DASO_PEER_CTAS_PER_SM");
-        v = (e && atoi(e) == 2) ? 2 : 1;
-    }
-    return v;
-}
+constexpr int kPT = 2048;
 
 struct PeerTmaLayout {   // byte offsets: NS input stages, then NO output buffers, then NS mbarriers
     uint32_t x, v, g, slot, in_bytes;    // inside an input stage
     uint32_t ox, ov, opack, out_bytes;   // inside an output buffer
 };
-template <int kPT>
 __host__ __device__ inline PeerTmaLayout peer_tma_layout(int ops, int G, int P, int wb) {
     PeerTmaLayout L{};
     uint32_t o = 0;
@@ -212,12 +193,12 @@ __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence
 
 // Input stage s is refilled as soon as its tile has been computed (outputs go to a separate
 // double-buffered output area), so the loads never wait for the NVLink stores to drain.
-template <int OPS, int WIRE, int G, int kPT>
+template <int OPS, int WIRE, int G>
 __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArgs pa, int NS) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
     const KernelArgs& a = pa.a;
-    const PeerTmaLayout L = peer_tma_layout<kPT>(OPS, G, a.P, wb);
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, a.P, wb);
     unsigned char* outs = smem + size_t(NS) * L.in_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(kPeerOut) * L.out_bytes);
     const bool leader = threadIdx.x == 0;
@@ -264,43 +245,42 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
         if (leader && k >= kPeerOut) bulk_wait_read<kPeerOut - 1>();   // output buffer ob drained
         mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err);
         __syncthreads();                                                 // also publishes the drain
-        for (int i = threadIdx.x * 8; i < kPT; i += kPeerThreads * 8) {
-            float x[8], v[8], g[8];
-            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
-            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.v, i, v);
-            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g, i, g);
+        const int i = threadIdx.x * 8;
+        float x[8], v[8], g[8];
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.v, i, v);
+        Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g, i, g);
 #pragma unroll
-            for (int q = 1; q < G; ++q) {
-                float t[8];
-                Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g + uint32_t(q) * kPT * 4, i, t);
+        for (int q = 1; q < G; ++q) {
+            float t[8];
+            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g + uint32_t(q) * kPT * 4, i, t);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) g[j] += t[j];                        // ascending local id (R18)
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
-                v[j] = fmaf(a.mu, v[j], d);
-                x[j] = fmaf(-a.lr, v[j], x[j]);
-            }
-            if constexpr ((OPS & OP_MERGE) != 0) {
-                float acc[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-                for (int p = 0; p < a.P; ++p) {
-                    float sv[8];
-                    Wire<WIRE>::template load_smem<8>(st + L.slot + uint32_t(p) * kPT * wb, i, sv);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[j] += sv[j] - x[j];
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
-            }
-            Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
-            Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
-            if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
+            for (int j = 0; j < 8; ++j) g[j] += t[j];                        // ascending local id (R18)
         }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
+            v[j] = fmaf(a.mu, v[j], d);
+            x[j] = fmaf(-a.lr, v[j], x[j]);
+        }
+        if constexpr ((OPS & OP_MERGE) != 0) {
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+            for (int p = 0; p < a.P; ++p) {
+                float sv[8];
+                Wire<WIRE>::template load_smem<8>(st + L.slot + uint32_t(p) * kPT * wb, i, sv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] += sv[j] - x[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
+        }
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
+        Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
+        if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
         fence_async_smem();
         __syncthreads();                                                 // stage s consumed, ob written
         if (leader) {
@@ -339,17 +319,16 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     }
 }
 
-template <int OPS, int WIRE, int G, int kPT>
+template <int OPS, int WIRE, int G>
 int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
-    const PeerTmaLayout L = peer_tma_layout<kPT>(OPS, G, pa.a.P, wb);
-    const int per_sm = peer_ctas_per_sm();
-    const int budget = (per_sm > 1 ? 100 : 210) * 1024 - kPeerOut * int(L.out_bytes);
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, pa.a.P, wb);
+    const int budget = 210 * 1024 - kPeerOut * int(L.out_bytes);
     const int NS = int(std::min<int64_t>(8, (budget - 64) / L.in_bytes));
     if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G, kPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     const size_t smem = size_t(NS) * L.in_bytes + size_t(kPeerOut) * L.out_bytes + 8 * size_t(NS);
@@ -361,8 +340,8 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
         const char* e = getenv("DASO_PEER_TMA_CTAS");
         ctas = e ? std::max(1, atoi(e)) : 0;
     }
-    const int grid = ctas > 0 ? std::min(ctas, sms * per_sm) : std::max(1, sms * per_sm - 16);
-    peer_tma_kernel<OPS, WIRE, G, kPT><<<dim3(unsigned(grid)), dim3(kPeerThreads), smem, s>>>(pa, NS);
+    const int grid = ctas > 0 ? std::min(ctas, sms) : std::max(1, sms - 16);
+    peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
 }
 
@@ -371,13 +350,7 @@ int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
     const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
                       reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
     // TMA unless the register path is forced (daso_kernel_impl(0))
-    if (current_kernel_impl() != 0 && al && pa.a.n >= peer_tile()) {
-        switch (peer_tile()) {
-            case 1024: return launch_peer_tma_t<OPS, WIRE, G, 1024>(pa, s, sms);
-            case 4096: return launch_peer_tma_t<OPS, WIRE, G, 4096>(pa, s, sms);
-            default: return launch_peer_tma_t<OPS, WIRE, G, 2048>(pa, s, sms);
-        }
-    }
+    if (current_kernel_impl() != 0 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
     return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
 }
 
