@@ -6,6 +6,7 @@ cool-down 5, B0 = 4, S0 = 1; plateau patterns Bernoulli(0.3) seed 7, all-true,
 all-false; G in {1, 2, 4, 8}) and exhaustive plateau patterns on short runs.
 """
 import itertools
+import math
 
 import pytest
 
@@ -63,3 +64,39 @@ def test_config_errors_match_oracle(bad):
     B0, S0, warm, cool, total, spe, G = bad
     with pytest.raises(ValueError):
         oracle_records(B0, S0, warm, cool, total, spe, G, [], 1)
+
+
+def test_random_configs_property_bit_exact():
+    """Property test: random valid configurations and plateau patterns, C++ == oracle."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+
+    @st.composite
+    def configs(draw):
+        B0 = draw(st.sampled_from([1, 2, 3, 4, 6, 8, 12, 16]))
+        chain, b = [], B0
+        while True:
+            chain.append(b)
+            if b == 1:
+                break
+            b = max(1, b // 2)
+        lcm = 1
+        for c in chain:
+            lcm = lcm * c // math.gcd(lcm, c)
+        spe = lcm * draw(st.integers(1, 3))
+        S0 = draw(st.integers(-1, B0))
+        total = draw(st.integers(1, 7))
+        warm = draw(st.integers(0, total))
+        cool = draw(st.integers(0, total - warm))
+        G = draw(st.integers(1, 8))
+        flags = draw(st.lists(st.integers(0, 1), min_size=total, max_size=total))
+        return B0, S0, warm, cool, total, spe, G, flags
+
+    @hyp.settings(max_examples=150, deadline=None)
+    @hyp.given(configs())
+    def check(c):
+        B0, S0, warm, cool, total, spe, G, flags = c
+        args = (B0, S0, warm, cool, total, spe, G, flags, total * spe + 3)
+        assert abi_records(*args) == oracle_records(*args)
+
+    check()
