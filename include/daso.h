@@ -133,7 +133,7 @@ typedef struct {
     float   momentum;         /* mu, P:172 uses 0.9 */
     float   weight_decay;     /* wd, P:172 uses 1e-4 */
     int32_t wire;             /* DASO_WIRE_BF16 (default) or DASO_WIRE_FP32 (R3) */
-    int32_t mode;             /* DASO_MODE_FAITHFUL or DASO_MODE_SHARDED */
+    int32_t mode;             /* DASO_MODE_FAITHFUL / _SHARDED / _FUSED / _NVLS (see the enum above) */
     int32_t check_finite;     /* 1 = fused non-finite flag in every update kernel */
     int32_t nccl_max_ctas;    /* >0: cap NCCL CTAs on the group (side-stream) comm to leave SMs to compute; 0 = NCCL default */
 } daso_config;
@@ -153,8 +153,8 @@ daso_status daso_get_unique_id(void* out128);
 daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S,
                       const daso_config* cfg, const void* nccl_uid128);
 
-/* n rounded up to a multiple of 64 * gpus_per_node: the bucket capacity the
- * sharded mode requires (shards of n_pad / G elements, 256-byte aligned). */
+/* n rounded up to a multiple of 64 * gpus_per_node: the bucket capacity the sharded,
+ * fused and nvls modes require (shards of n_pad / G elements, 256-byte aligned). */
 size_t daso_padded_numel(size_t n, int gpus_per_node);
 
 /* Attach the caller's flat fp32 buckets ("buffer packaging"): params x[n],
@@ -165,8 +165,11 @@ size_t daso_padded_numel(size_t n, int gpus_per_node);
  * with the node peers, which then read g and write x of this rank directly.
  * Caller-owned; they must stay alive and unmoved until daso_finalize.  x must be
  * identical on every rank (R17) and v zero-initialised by the caller.  The library
- * allocates its ring of exchange slots here: [P][n_pad] wire elements (n_pad = n
- * rounded up to 64 * G).  Errors: DASO_ERR_PROTOCOL (bound twice), DASO_ERR_ARGUMENT. */
+ * allocates its exchange slot here: [P][seg] wire elements (seg = n_pad in the faithful
+ * mode, n_pad / G otherwise; n_pad = n rounded up to 64 * G).  Errors:
+ * DASO_ERR_PROTOCOL (bound twice; DASO_MODE_NVLS with G > 1, which needs
+ * daso_alloc_bind), DASO_ERR_ARGUMENT (null, n = 0, misaligned, not a device allocation
+ * in the fused mode), DASO_ERR_CUDA / DASO_ERR_NCCL. */
 daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n);
 
 /* Allocate the flat buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed) in
@@ -199,8 +202,11 @@ daso_status daso_global_merge(daso_ctx* c, void* stream);
  * advance the schedule (record in *out if non-null), node all-reduce of g, the fused
  * update (+ Eq. (1) merge if due) (+ wire pack if this rank sends) kernel, node
  * broadcast after a merge, side-stream group all-gather for a send, and — blocking
- * — the average kernel and broadcast.  `lr` is this batch's learning rate;
- * `plateau` as in daso_sched_next. */
+ * — the average kernel and broadcast.  Sharded / fused / nvls modes run the same batch
+ * element-sharded over the node; fused and nvls put the whole node tier
+ * in one kernel.  `lr` is this batch's learning rate; `plateau` as in daso_sched_next.
+ * Errors: DASO_ERR_PROTOCOL (not bound; schedule/flight-state mismatch), asynchronous
+ * DASO_ERR_CUDA / DASO_ERR_NCCL from earlier work. */
 daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out);
 
 /* ----- backward-overlapped local sync ("The local networks utilize
