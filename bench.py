@@ -321,6 +321,12 @@ def run_ours(a):
     if traffic is not None:
         roofline["traffic"] = traffic
         roofline["traffic_source"] = tsrc
+        # DRAM bytes ncu saw inside one launch / this run's launch time: part of each launch's
+        # writes (~25 % for K1) is still dirty in L2 when the kernel ends and drains afterwards,
+        # so "frac" (algorithmic bytes) can read a little above 1 while this stays below it.
+        ms_launch = tr["kernel_ms"] / max(tr["kernel_launches"], 1)
+        if ms_launch > 0:
+            roofline["frac_in_kernel_dram"] = traffic / (ms_launch * 1e-3) / 1e9 / peak
     if a.mode in ("fused", "nvls") and G > 1:
         # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
         # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)
