@@ -230,3 +230,23 @@ def test_full_size_microbench_sampled(tmp_path, mode, wire):
             rms = np.sqrt(np.mean(xo ** 2))
             assert np.all(np.abs(tr[k] - xo) <= tol * (np.abs(xo) + rms)), (rk, k)
             assert np.linalg.norm(tr[k] - xo) <= tol * np.linalg.norm(xo)
+
+
+def test_config5_schedule_through_daso_step(tmp_path):
+    """Config 5: 1000 batches = 50 epochs x 20, warm-up 5, cool-down 5, B0 = 4,
+    S0 = 1, plateau flags Bernoulli(0.3) (seed 7): every record daso_step returns on every rank
+    equals the oracle's schedule bit for bit (2x2 on 4 GPUs; 2x4 needs 8)."""
+    flags = "".join(str(f) for f in synthetic.plateau_pattern(50, 0.3))
+    args = ["--P", "2", "--G", "2", "--B", "4", "--S", "1", "--warmup", "5", "--cooldown", "5", "--epochs", "50",
+            "--spe", "20", "--steps", "1000", "--flags", flags, "--dim", "64", "--mode", "fused"]
+    ranks = run_world(str(tmp_path), 4, args)
+    cfg = SchedConfig(B_init=4, S_init=1, warmup_epochs=5, cooldown_epochs=5, total_epochs=50, steps_per_epoch=20,
+                      gpus_per_node=2)
+    from oracle.schedule import run_schedule
+    ref = [r.as_dict() for r in run_schedule(cfg, 1000, [int(c) for c in flags])]
+    for f in ranks:
+        fields = [str(s) for s in f["rec_fields"]]
+        got = [dict(zip(fields, (int(v) for v in row))) for row in f["recs"]]
+        assert got == ref
+    for j in range(2):   # node replicas identical at every one of the 1000 batches
+        np.testing.assert_array_equal(ranks[2 * j + 1]["cks"], ranks[2 * j]["cks"])
