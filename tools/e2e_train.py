@@ -62,6 +62,45 @@ def HMSA(classes: int):
     return _HMSA()
 
 
+def train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank):
+    """The whole DASO control loop on real (synthetic-data) losses: per epoch, the mean training
+    loss over all ranks feeds the plateau detector (daso_plateau_*); a plateau decays the
+    LR (daso_lr_at) and is passed to the next epoch's first daso_step, which halves or
+    resets B and S.  Prints one JSON record per epoch on rank 0."""
+    import torch
+    import torch.distributed as dist
+    import paper_2104_05588_b200 as daso
+    det = daso.PlateauDetector(a.patience, a.threshold)
+    n_plateaus, plateau_next, k = 0, 0, 0
+    base_lr = a.lr / world                      # peak = base * world (P:172)
+    for e in range(a.train_epochs):
+        total = torch.zeros((), device=images.device)
+        for i in range(a.steps_per_epoch):
+            lr = daso.daso_lr_at(k, a.steps_per_epoch, base_lr, world, a.lr_warmup_epochs, a.lr_factor, n_plateaus)
+            flat.g.zero_()
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = loss_fn(net(images), labels)
+            loss.backward()
+            rec = ctx.step(lr, plateau_next if i == 0 else 0)
+            total += loss.detach().float()
+            k += 1
+        mean = total / a.steps_per_epoch
+        if world > 1:
+            t = torch.tensor([float(mean.item())], dtype=torch.float64)
+            dist.all_reduce(t)
+            mean_loss = float(t.item()) / world
+        else:
+            mean_loss = float(mean.item())
+        plateau_next = det.update(mean_loss)
+        n_plateaus += plateau_next
+        if rank == 0:
+            print(json.dumps({"epoch": e, "mean_loss": mean_loss, "lr": lr, "plateau": plateau_next,
+                              "phase": rec["phase"], "B": rec["B"], "S": rec["S"], "syncs": rec["n_syncs"]}),
+                  flush=True)
+    if not ctx.check_finite():
+        raise RuntimeError("non-finite parameters")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", choices=["resnet50", "hmsa"], default="resnet50")
@@ -75,6 +114,14 @@ def main():
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--overlap", action="store_true",
                     help="faithful mode: node all-reduce in buckets overlapped with backward (N2)")
+    ap.add_argument("--train-epochs", type=int, default=0,
+                    help="instead of timing: train this many epochs with the full loop of P:97-99/P:162/P:172 — "
+                         "epoch-mean loss -> plateau detector -> LR decay and DASO B/S halving (N4)")
+    ap.add_argument("--steps-per-epoch", type=int, default=8)
+    ap.add_argument("--patience", type=int, default=2)
+    ap.add_argument("--threshold", type=float, default=0.01)
+    ap.add_argument("--lr-warmup-epochs", type=int, default=1)
+    ap.add_argument("--lr-factor", type=float, default=0.5)
     a = ap.parse_args()
 
     import torch
@@ -129,8 +176,12 @@ def main():
             G = G_node
             P, B, S = world // G, 4, 1
         uid = daso.rendezvous_unique_id() if world > 1 else daso.daso_get_unique_id()
-        ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
-                             total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode)
+        if a.train_epochs:
+            ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
+                                 total_epochs=max(a.train_epochs, 2), steps_per_epoch=a.steps_per_epoch, mode=a.mode)
+        else:
+            ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
+                                 total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode)
         flat = daso.FlatParams(model.parameters(), gpus_per_node=G)
         ctx.bind(flat.x, flat.g, flat.v, flat.n)
         overlap = daso.OverlappedLocalSync(ctx, flat) if a.overlap else None
@@ -151,6 +202,13 @@ def main():
         else:
             ctx.step(a.lr)
         return loss
+
+    if a.train_epochs and ctx is not None:
+        train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank)
+        ctx.finalize()
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     for _ in range(a.warmup):
         step()
