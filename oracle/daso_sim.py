@@ -93,16 +93,3 @@ def simulate(P: int, G: int, cfg: SchedConfig, steps: int, x0: np.ndarray,
         out["trace"] = hist
     return out
 
-
-def flat_sync_sgd(W: int, steps: int, x0: np.ndarray,
-                  grad_fn: Callable[[int, int, np.ndarray], np.ndarray],
-                  lr: float, mu: float, wd: float) -> np.ndarray:
-    """Synchronous data-parallel SGD (the paper's baseline notion, "perform a
-    forward-backward pass on each network instance ... then synchronize ... via a
-    global averaging operation"): one replica, gradient = mean over all W ranks."""
-    x = np.array(x0, dtype=np.float64, copy=True)
-    v = np.zeros_like(x)
-    for k in range(steps):
-        gbar = numerics.average([grad_fn(r, k, x) for r in range(W)])
-        x, v = sgd.sgd_step(x, v, gbar, lr, mu, wd)
-    return x

@@ -152,3 +152,56 @@ def test_toy_gradient_finite_differences():
     Xs, ys = np.split(X.astype(np.float64)[:4], 2), np.split(y.astype(np.float64)[:4], 2)
     np.testing.assert_allclose(toy.grad(w, X[:4], y[:4]), 0.5 * (toy.grad(w, Xs[0], ys[0]) + toy.grad(w, Xs[1], ys[1])),
                                rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# Hand-derived pins of the bf16 wire THROUGH simulate ("parameters are cast to a
+# 16-bit datatype representation during buffer packaging ... cast back to their original
+# datatype"; Eq. (1)).  2 nodes x 1 GPU, mu = wd = 0, lr = 1, and a gradient
+# g = w - target so that every local state is an exact, hand-chosen value.  The values
+# are dyadic with more than 8 significant bits, so bf16 RNE changes them, incl. both tie
+# directions; the expected numbers below were derived by hand (bf16 keeps 8 significant
+# bits: 1 + 3*2^-9 -> 1 + 2^-7 (round up), 1 + 2^-8 -> 1 (tie, to even), 0.5 + 2^-10 -> 0.5
+# (quarter ulp, down), 3 + 2^-7 -> 3 (tie, to even), fl64(1/3) -> 0.333984375).
+# A composition mistake (casting the local state instead of the stale snapshot, casting
+# after the merge, dropping the own snapshot, a wrong S weight) changes every number.
+_T0 = [[1 + 3 * 2 ** -9, 1 + 2 ** -8, 1 / 3], [0.5 + 2 ** -10, 3 + 2 ** -7, 1 / 3]]   # after batch 0
+_T1 = [[4.0, 2.0, 4.0], [1.0, -1.0, 4.0]]                                               # after batch 1
+
+
+def _target_grad(r, k, w):
+    return w - np.array((_T0 if k == 0 else _T1)[r])
+
+
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+def test_bf16_wire_merge_hand_pin(wire):
+    """B = 2, S = 1: send after batch 0, Eq. (1) merge after batch 1's update:
+        x = (2S x_local + sum_i wire(x_i,0)) / (2S + P) = (2 x_local + s_0 + s_1) / 4."""
+    cfg = SchedConfig(B_init=2, S_init=1, total_epochs=1, steps_per_epoch=8)
+    out = daso_sim.simulate(2, 1, cfg, 2, np.zeros(3), _target_grad, 1.0, 0.0, 0.0, wire=wire, trace=True)
+    assert out["records"][0].send == 1 and out["records"][1].merge == 1
+    np.testing.assert_array_equal(out["trace"][0][0], _T0[0])          # batch 0: plain local updates
+    np.testing.assert_array_equal(out["trace"][0][1], _T0[1])
+    if wire == "bf16":
+        # snapshots bf16: node 0 [1.0078125, 1.0, 0.333984375], node 1 [0.5, 3.0, 0.333984375]
+        want = [[(8 + 1.0078125 + 0.5) / 4, (4 + 1.0 + 3.0) / 4, (8 + 2 * 0.333984375) / 4],
+                [(2 + 1.0078125 + 0.5) / 4, (-2 + 1.0 + 3.0) / 4, (8 + 2 * 0.333984375) / 4]]
+        assert want[0] == [2.376953125, 2.0, 2.1669921875]                # the hand values
+        assert want[1] == [0.876953125, 0.5, 2.1669921875]
+    else:
+        # fp32 wire (P:88 "casting is not beneficial"): the snapshots are the exact states
+        want = [[(8 + 1.005859375 + 0.5009765625) / 4, (4 + 1.00390625 + 3.0078125) / 4, (8 + 2 / 3) / 4],
+                [(2 + 1.005859375 + 0.5009765625) / 4, (-2 + 1.00390625 + 3.0078125) / 4, (8 + 2 / 3) / 4]]
+        assert want[0][:2] == [2.376708984375, 2.0029296875]
+    for r in range(2):
+        np.testing.assert_allclose(out["trace"][1][r], want[r], rtol=0, atol=1e-15)
+
+
+def test_bf16_wire_blocking_average_hand_pin():
+    """B = 1, S = 0 (blocking, Fig. 3, P:83 / P:86): after batch 0 both nodes hold the
+    plain mean of the two bf16 snapshots: [(1.0078125 + 0.5)/2, (1 + 3)/2, 0.333984375]."""
+    cfg = SchedConfig(B_init=1, S_init=0, total_epochs=1, steps_per_epoch=8)
+    out = daso_sim.simulate(2, 1, cfg, 1, np.zeros(3), _target_grad, 1.0, 0.0, 0.0, wire="bf16", trace=True)
+    assert out["records"][0].send == 1 and out["records"][0].blocking == 1
+    for r in range(2):
+        np.testing.assert_array_equal(out["trace"][0][r], [0.75390625, 2.0, 0.333984375])
