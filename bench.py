@@ -64,6 +64,12 @@ def parse():
     ap.add_argument("--compute-ms", type=float, default=0.0,
                     help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
                          "the global exchange the next batch's compute hides")
+    ap.add_argument("--overlap-compute-ms", type=float, default=20.0,
+                    help="fwd/bwd stand-in per batch inside the hidden-fraction cycles (P > 1)")
+    ap.add_argument("--cycles", type=int, default=8, help="B-cycles per leg of the hidden-fraction measurement")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline table (N=1)")
+    ap.add_argument("--ref-div", type=int, default=4,
+                    help="reference arm: oracle sample = n / ref-div parameters per step (scaled per parameter)")
     return ap.parse_args()
 
 
@@ -231,7 +237,10 @@ def run_reference(a):
         return
     P, G = topology(a, world)
     from oracle import bench as obench
-    n_sample = max(1 << 16, a.n // 16)
+    # n/4 by default: at that size every fp64 state vector (51 MB) is far larger than the host's
+    # caches, so the per-parameter cost is the full-size one (a 1/16 sample fit in cache and read
+    # ~2x faster than full size in round 1)
+    n_sample = max(1 << 16, a.n // max(1, a.ref_div))
     r = obench.time_sync_path(P, G, a.B, a.S, n_sample, a.steps, warmup=a.warmup, lr=a.lr, wire=a.wire)
     gbs = 4.0 * n_sample * P * G / r["s_per_step"] / 1e9
     sample = (f"oracle.daso_sim (numpy fp64, 1 core of {os.cpu_count()}) on {n_sample:,} of {a.n:,} params per "
@@ -244,6 +253,114 @@ def run_reference(a):
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def kernel_table(n: int, peak: float, iters: int = 30, warmup: int = 5) -> dict:
+    """Per-kernel HBM roofline of every fused kernel on the sync path at n parameters (SURVEY §8(d),
+    DESIGN.md §6), launched through the C ABI on resident buffers, CUDA events on the launching
+    stream around each launch, a 256 MB read between launches so each starts from a cold, clean
+    L2.  achieved = algorithmic bytes per launch / mean launch time; frac = achieved / peak."""
+    import torch
+    import paper_2104_05588_b200 as daso
+    stride = daso.daso_padded_numel(n, 8)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = (torch.randn(stride, device="cuda", generator=gen) * 0.02)[:n]
+    v = torch.zeros(stride, device="cuda")[:n]
+    g = (torch.randn(stride, device="cuda", generator=gen) * 0.01)[:n]
+    slot = (torch.randn(8, stride, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
+    pk = torch.zeros(stride, dtype=torch.bfloat16, device="cuda")
+    wb = 2
+    cases = {
+        "K1_update": (lambda: daso.daso_k_update(x, v, g, 1e-3, 0.9, 1e-4, 0.5), 20),
+        "K2_update_pack": (lambda: daso.daso_k_update(x, v, g, 1e-3, 0.9, 1e-4, 0.5, pack_out=pk), 20 + wb),
+        "K3_update_merge_P2": (lambda: daso.daso_k_update_merge(x, v, g, 1e-3, 0.9, 1e-4, 0.5, slot[:2], 1), 20 + 2 * wb),
+        "K3_update_merge_pack_P2": (lambda: daso.daso_k_update_merge(x, v, g, 1e-3, 0.9, 1e-4, 0.5, slot[:2], 1,
+                                                                      pack_out=pk), 20 + 3 * wb),
+        "K3_update_merge_P8": (lambda: daso.daso_k_update_merge(x, v, g, 1e-3, 0.9, 1e-4, 0.5, slot[:8], 1), 20 + 8 * wb),
+        "K4_average_P2": (lambda: daso.daso_k_average(x, slot[:2]), 2 * wb + 4),
+        "K4_average_P8": (lambda: daso.daso_k_average(x, slot[:8]), 8 * wb + 4),
+        "pack_only": (lambda: daso.daso_k_pack(x, pk), 4 + wb),
+    }
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    rows = {}
+    for name, (fn, bpp) in cases.items():
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        stream = torch.cuda.current_stream()
+        for e0, e1 in ev:
+            flush.sum()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        us = sorted(e0.elapsed_time(e1) * 1e3 for e0, e1 in ev)
+        mean = sum(us) / len(us)
+        gbs = bpp * n / (mean * 1e-6) / 1e9
+        rows[name] = {"bytes_per_param": bpp, "bytes_per_launch": bpp * n, "us_mean": mean, "us_p10": us[len(us) // 10],
+                      "us_p90": us[(9 * len(us)) // 10], "achieved_gbs": gbs, "frac": gbs / peak}
+    return rows
+
+
+def pct(xs, q):
+    xs = sorted(xs)
+    return xs[min(len(xs) - 1, int(q * len(xs)))] if xs else None
+
+
+def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle):
+    """SURVEY §8(d) hidden fraction: hidden = 1 - (T_with - T_without) / T_AG,alone, per B-cycle.
+    One cycle = B batches of [fwd/bwd stand-in (bf16 GEMMs) ; gradient refresh ; daso_step], timed by
+    CUDA events on the compute stream from the cycle's first batch to the end of its last.  In
+    steady state every cycle contains exactly one merge, whose batch makes the compute stream wait
+    for its exchange (S <= B batches after the send), so each cycle's time includes exactly one
+    exchange's exposed part.  T_without: the same cycles with the group all-gather suppressed (daso_set_exchange(0)).
+    T_AG,alone: the all-gather alone (daso_exchange_alone)."""
+    import torch
+
+    def leg(enabled):
+        ctx.set_exchange(enabled)
+        for _ in range(2 * a.B):                   # settle into the cycle with this setting
+            compute()
+            g.copy_(g_src)
+            ctx.step(a.lr)
+        while ctx.query()["batch_in_cycle"] != a.B - 1:
+            compute()
+            g.copy_(g_src)
+            ctx.step(a.lr)
+        torch.cuda.synchronize()
+        barrier(world)
+        ts = []
+        for _ in range(a.cycles):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(a.B):
+                compute()
+                g.copy_(g_src)
+                ctx.step(a.lr)
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        return [e0.elapsed_time(e1) for e0, e1 in ts]
+
+    t_with = leg(True)
+    t_without = leg(False)
+    ctx.set_exchange(True)
+    torch.cuda.synchronize()
+    barrier(world)
+    t_ag = ctx.exchange_alone(10)
+    w_med = max_over_ranks(statistics.median(t_with), world)
+    wo_med = max_over_ranks(statistics.median(t_without), world)
+    t_ag = max_over_ranks(t_ag, world)
+    exposed = max(0.0, w_med - wo_med)
+    hidden = 1.0 - exposed / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
+    return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); medians over cycles, "
+                   "max over ranks",
+            "cycles": a.cycles, "compute_ms_per_batch": a.overlap_compute_ms,
+            "T_cycle_with_ms": w_med, "T_cycle_without_ms": wo_med,
+            "T_cycle_with_p10_p90": [pct(t_with, 0.1), pct(t_with, 0.9)],
+            "T_cycle_without_p10_p90": [pct(t_without, 0.1), pct(t_without, 0.9)],
+            "T_AG_alone_ms": t_ag, "exchanges_per_cycle": n_exch_per_cycle, "hidden_fraction": hidden}
 
 
 def run_ours(a):
@@ -288,7 +405,7 @@ def run_ours(a):
     torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    kinds = {"plain": 0, "send": 0, "merge": 0, "blocking": 0}
+    kind_of = []
     with ClockSampler(local) as clk:
         for k in range(a.steps):
             g.copy_(g_src)
@@ -297,7 +414,11 @@ def run_ours(a):
             ev0[k].record(stream)
             r = ctx.step(a.lr)
             ev1[k].record(stream)
-            kinds["blocking" if r["blocking"] else "merge" if r["merge"] else "send" if r["send"] else "plain"] += 1
+            # the batch kind that EXECUTED: with P = 1 the global tier is disabled (R12), so every
+            # batch is a plain update whatever the schedule record says
+            kind_of.append("plain" if P == 1 else "blocking" if r["blocking"] else
+                           "merge+send" if (r["merge"] and r["send"]) else "merge" if r["merge"] else
+                           "send" if r["send"] else "plain")
         torch.cuda.synchronize()
     barrier(world)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in zip(ev0, ev1)]
@@ -352,6 +473,19 @@ def run_ours(a):
         phases["exch_gbs"] = tr["exch_bytes"] / (tr["exch_ms"] * 1e-3) / 1e9
         phases["hidden_fraction"] = max(0.0, 1.0 - tr["wait_ms"] / tr["exch_ms"])
     phases["p50_step_ms"] = statistics.median(step_ms)
+    kinds = {}
+    for kd in sorted(set(kind_of)):
+        xs = [t for t, kk in zip(step_ms, kind_of) if kk == kd]
+        kinds[kd] = {"count": len(xs), "ms_p10": pct(xs, 0.1), "ms_p50": statistics.median(xs), "ms_p90": pct(xs, 0.9)}
+    kinds_max = {}
+    for kd, d in kinds.items():   # max over ranks of each percentile
+        kinds_max[kd] = {k: (max_over_ranks(v, world) if k.startswith("ms") else v) for k, v in d.items()}
+
+    # ---- §8(d) hidden fraction of the global exchange (P > 1) -------------------------------------
+    overlap = None
+    if P > 1:
+        nx = 1 if a.S > 0 else a.B          # exchanges issued per B-cycle
+        overlap = overlap_cycles(ctx, a, g, g_src, stream, world, make_compute(a.overlap_compute_ms, dev), nx)
 
     # ---- e2e through the C ABI with host buffers (daso_step_host) -------------------------------
     e2e = None
@@ -372,8 +506,20 @@ def run_ours(a):
         barrier(world)
         te = max_over_ranks(e0.elapsed_time(e1), world) / k2
         e2e = {"value": 4.0 * n * world / (te * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": te,
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4}
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4,
+               "what": "daso_step_host per batch: the step's gradients copied in from pinned host memory, the "
+                       "whole sync path, the 4-byte non-finite flag (the step's result) copied back; the "
+                       "parameters stay device-resident, as in training (the next forward reads them there)"}
     ctx.finalize()
+
+    kernels = None
+    if world == 1 and not a.no_kernels:
+        with ClockSampler(local) as kclk:
+            kernels = kernel_table(n, peak)
+        kernels = {"n_params": n, "peak_gbs": peak, "peak_source": peak_src, "clocks": kclk.summary(),
+                   "timing": "CUDA events on the launching stream around each launch, 256 MB L2 flush between "
+                             "launches, 30 launches after 5 warm-up; achieved = algorithmic bytes / mean time",
+                   "kernels": kernels}
 
     if rank != 0:
         return
@@ -385,8 +531,13 @@ def run_ours(a):
                        "wire": a.wire, "parallelism": f"daso {P} virtual nodes x {G} GPUs",
                        "l2": "flushed before every timed step (untimed read of a 256 MB buffer after the "
                              "gradient refresh); the inputs (x, v, g = 307 MB) also exceed the 126 MB L2",
-                       "value_def": "4 B x n params x N GPUs / ms_per_step", "step_kinds": kinds,
+                       "value_def": "4 B x n params x N GPUs / ms_per_step",
+                       "timed_window": "per batch: daso_step on the compute stream (node tier, fused kernel, "
+                                       "exchange issue and the wait at a merge); the side-stream all-gather "
+                                       "overlaps the untimed refresh/flush between steps -- the full-cycle "
+                                       "timing with the exchange inside the window is `overlap`",
                        "compute_ms_between_steps": a.compute_ms},
+            "step_kinds": kinds_max, "overlap": overlap, "kernels": kernels,
             "roofline": roofline, "phases": phases, "gpu_launches": launches_total,
             "gpu_launches_per_rank": tr["kernel_launches"],
             "clocks": clk.summary(), "e2e": e2e, "finite": finite}

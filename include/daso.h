@@ -174,9 +174,11 @@ daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n);
 
 /* Allocate the flat buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed) in
  * library-owned memory and bind them; returns the device pointers (owned by the library,
- * valid until daso_finalize).  x and g are NCCL symmetric memory (ncclMemAlloc) registered
- * as windows on the node communicator, which DASO_MODE_NVLS requires for its multicast
- * addresses; collective over the node.  Errors: as daso_bind; DASO_ERR_CONFIG if the node
+ * valid until daso_finalize).  DASO_MODE_NVLS (G > 1): x and g are NCCL symmetric memory
+ * (ncclMemAlloc) registered as windows on the node communicator, which NVLS requires for
+ * its multicast addresses; every other mode: cudaMalloc (what the fused mode's CUDA IPC
+ * export needs — use this when the caller's allocator hands out cuMem memory, e.g.
+ * PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True).  Collective over the node.  Errors: as daso_bind; DASO_ERR_CONFIG if the node
  * has no NVLS multicast support (NVLS mode). */
 daso_status daso_alloc_bind(daso_ctx* c, size_t n, float** x, float** g, float** v);
 
@@ -244,6 +246,21 @@ typedef struct {
 daso_status daso_trace_enable(daso_ctx* c, int on);
 daso_status daso_trace_read(daso_ctx* c, daso_trace* out, int reset);
 
+/* ----- measurement knobs (bench.py, SURVEY §8(d) hidden fraction) -----
+ * daso_set_exchange(c, 0) suppresses the side-stream group all-gather (the events that
+ *   order it are still recorded): the T_step,without leg of hidden = 1 - (T_with -
+ *   T_without) / T_AG,alone.  Nodes are then NOT synchronised — never use it in training.
+ *   1 re-enables; any other value only queries.  Returns the previous setting (-1: null c).
+ * daso_exchange_alone(c, iters, &ms): collective over the group (every rank must call it);
+ *   runs the group all-gather of the bound slot `iters` times back to back on the side
+ *   stream with nothing else running (T_AG,alone), returns the mean ms per all-gather
+ *   (CUDA events on the side stream; one untimed warm-up).  Synchronises the device.  The
+ *   slot's rows are overwritten with every member's current packed row, as in a real send.
+ *   0 ms if P = 1.  Errors: DASO_ERR_PROTOCOL (exchange in flight, virtual cluster),
+ *   DASO_ERR_ARGUMENT, DASO_ERR_NCCL / CUDA. */
+int daso_set_exchange(daso_ctx* c, int enabled);
+daso_status daso_exchange_alone(daso_ctx* c, int iters, double* ms_out);
+
 /* Last schedule record and whether an exchange is in flight (host-only, no sync). */
 daso_status daso_query(const daso_ctx* c, daso_record* last);
 /* Synchronise `stream` and read (then clear) the fused non-finite flag:
@@ -254,6 +271,40 @@ daso_status daso_finalize(daso_ctx* c);
 const char* daso_last_error(const daso_ctx* c);
 /* Topology of the ctx: P, G, node, local. */
 daso_status daso_topology(const daso_ctx* c, int* P, int* G, int* node, int* local);
+
+/* -------------------------------------------- virtual cluster on ONE GPU (parity harness)
+ * W = world virtual ranks (P = world / gpus_per_node nodes x G), all on the CUDA device
+ * current at create, each a full ctx running the product batch (daso_step_ex and the same
+ * kernels); only the transport is emulated:
+ *   - node tier (DASO_MODE_FUSED, G > 1): the fused kernel of every rank reads its node
+ *     peers' g and writes their x directly in the sibling ranks' buffers on the same GPU
+ *     (Fig. 2 / Fig. 4).  The G kernels of a node run one after another on one
+ *     stream; the node's barrier signals are pre-set so no launch ever waits on another;
+ *   - global tier: the group all-gather is a device-to-device copy of every
+ *     packed row into every group member's slot, issued on `stream` after all ranks' batch;
+ *     blocking syncs finish with the average (Fig. 3) after that copy.
+ * Stream order provides what the barriers and events provide across GPUs, and the shards
+ * are disjoint, so every rank computes what it computes on its own GPU.
+ * Modes: DASO_MODE_FUSED with any G <= 8; DASO_MODE_FAITHFUL / _SHARDED only with G = 1
+ * (their node tier is NCCL, which cannot loop back on one GPU); else DASO_ERR_CONFIG.
+ * Buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed; x must be set identical on
+ * every rank, R17) are owned by the cluster.  cfg->rank is ignored.
+ * daso_vcluster_create: errors as daso_init (CONFIG / RANGE / ARGUMENT), DASO_ERR_CUDA.
+ * daso_vcluster_buffers: a rank's device pointers (nullable outputs); DASO_ERR_RANGE.
+ * daso_vcluster_rank: the rank's ctx (for daso_trace_* / daso_query / daso_check_finite;
+ *   never daso_finalize it), NULL if out of range.
+ * daso_vcluster_step: one batch of every rank in rank order (gradients already in each g);
+ *   out (nullable) receives world records.  Errors as daso_step; DASO_ERR_PROTOCOL if the
+ *   ranks' schedules disagree.
+ * daso_vcluster_destroy: synchronise, finalize every rank, free the buckets. */
+typedef struct daso_vcluster daso_vcluster;
+daso_status daso_vcluster_create(daso_vcluster** out, int world, int gpus_per_node, int B, int S,
+                                 const daso_config* cfg, size_t n);
+daso_status daso_vcluster_buffers(daso_vcluster* v, int rank, float** x, float** g, float** vb);
+daso_ctx* daso_vcluster_rank(daso_vcluster* v, int rank);
+daso_status daso_vcluster_step(daso_vcluster* v, float lr, int plateau, void* stream, daso_record* out);
+daso_status daso_vcluster_destroy(daso_vcluster* v);
+const char* daso_vcluster_last_error(const daso_vcluster* v);
 
 /* ------------------------------------------------------ kernel entry points
  * Stream-ordered launches of the fused sm_100a kernels on caller memory, without

@@ -119,6 +119,16 @@ _SIG = {
                                  C.c_int, C.c_void_p]),
     "daso_k_checksum": (C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "daso_kernel_impl": (C.c_int, [C.c_int]),
+    "daso_set_exchange": (C.c_int, [C.c_void_p, C.c_int]),
+    "daso_exchange_alone": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
+    "daso_vcluster_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(Config),
+                                       C.c_size_t]),
+    "daso_vcluster_buffers": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_void_p)]),
+    "daso_vcluster_rank": (C.c_void_p, [C.c_void_p, C.c_int]),
+    "daso_vcluster_step": (C.c_int, [C.c_void_p, C.c_float, C.c_int, C.c_void_p, C.POINTER(Record)]),
+    "daso_vcluster_destroy": (C.c_int, [C.c_void_p]),
+    "daso_vcluster_last_error": (C.c_char_p, [C.c_void_p]),
 }
 EXPORTED = sorted(_SIG)
 

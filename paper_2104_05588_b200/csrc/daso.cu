@@ -26,6 +26,8 @@
 
 #include "daso_internal.h"
 
+struct daso_vcluster;
+
 struct daso_ctx {
     int world = 0, G = 0, P = 0, rank = 0, node = 0, local = 0;
     int device = 0;
@@ -47,6 +49,7 @@ struct daso_ctx {
 
     bool inflight = false;
     int infl_group = -1, infl_S = 0;
+    bool exch_enabled = true;   // daso_set_exchange(0): timing knob, the group all-gather is skipped
 
     // fused mode: node peers' buffers mapped through CUDA IPC (NVLink peer memory)
     float* peer_x[daso::kMaxPeers] = {};
@@ -56,11 +59,20 @@ struct daso_ctx {
     unsigned long long epoch = 0;
     std::vector<void*> ipc_opened;
 
-    // NVLS mode: library-owned buckets in NCCL symmetric memory (daso_alloc_bind)
-    bool owns_buckets = false;
+    // library-owned buckets (daso_alloc_bind): NCCL symmetric memory for NVLS, cudaMalloc otherwise
+    void* own_nccl[3] = {};
+    void* own_cuda[3] = {};
     daso::NvlsBuckets nvls{};
     float* x_mc = nullptr;   // multicast (NVLS) address of x
     float* g_mc = nullptr;   // multicast (NVLS) address of g
+
+    // virtual cluster (daso_vcluster_*): this ctx is one of W virtual ranks on ONE GPU; the
+    // group all-gather and the blocking tail are run by the cluster driver after every rank's
+    // batch (loopback transport), the node tier's peers are the sibling ranks' buffers
+    daso_vcluster* vc = nullptr;
+    bool vc_sent = false, vc_blocking = false;
+    int vc_group = -1;
+    unsigned long long* vc_node_sig = nullptr;   // the node's [G][2G+2] signal block (local 0 pre-sets it)
 
     daso_record last{};
     std::string err;
@@ -144,6 +156,7 @@ daso::KernelArgs base_args(daso_ctx* c, int64_t off, int64_t len, float lr) {
     a.slot_stride = c->seg;
     a.P = c->P;
     a.flag = c->cfg.check_finite ? c->d_flag : nullptr;
+    a.err = c->d_flag;
     return a;
 }
 
@@ -202,9 +215,13 @@ int launch(daso_ctx* c, int ops, const daso::KernelArgs& a, cudaStream_t s) {
 // Non-blocking global exchange: after the packing kernel on the compute
 // stream, the side stream runs the in-place group all-gather of the slot.
 daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
+    if (c->vc) {   // virtual cluster: the driver copies every packed row after all ranks ran
+        c->vc_sent = true;
+        return DASO_OK;
+    }
     CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
-    {
+    if (c->exch_enabled) {
         Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(c->seg) * double(c->wire_bytes));
         NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
                                   c->side));
@@ -214,6 +231,7 @@ daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
 }
 
 daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
+    if (c->vc) return DASO_OK;   // virtual cluster: the loopback copies precede on the same stream
     Span sp(c, s, PH_WAIT, 0.0);
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));
     return DASO_OK;
@@ -225,6 +243,51 @@ daso_status node_bcast(daso_ctx* c, int root, cudaStream_t s) {
     Span sp(c, s, PH_NODE, 4.0 * double(c->n));
     NCCL_TRY(c, ncclBroadcast(c->x, c->x, size_t(c->n), ncclFloat32, root, c->node_comm, s));
     return DASO_OK;
+}
+
+// ---- blocking tails (Fig. 3 average + Fig. 4 re-publish, on the critical path) ------------
+// Split out of the step functions so the virtual-cluster driver can run them after its
+// loopback all-gather (daso_vcluster_step).
+daso_status faithful_blocking_tail(daso_ctx* c, int group, cudaStream_t s) {
+    if (c->local == group) {
+        STATUS_TRY(wait_exchange(c, s));
+        daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
+        av.den = float(c->P);
+        KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+    }
+    return node_bcast(c, group, s);
+}
+
+daso_status shard_blocking_tail(daso_ctx* c, cudaStream_t s) {   // sharded / fused with G = 1
+    const int64_t off = int64_t(c->local) * c->seg;
+    STATUS_TRY(wait_exchange(c, s));
+    daso::KernelArgs av = base_args(c, off, c->seg, 0.f);
+    av.den = float(c->P);
+    KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+    return DASO_OK;
+}
+
+daso_status fused_blocking_tail(daso_ctx* c, cudaStream_t s) {
+    const int64_t sh = c->seg, off = int64_t(c->local) * sh;
+    STATUS_TRY(shard_blocking_tail(c, s));
+    // re-publish the averaged shard to the node peers (NVLink copies) ...
+    for (int q = 0; q < c->G; ++q) {
+        if (q == c->local) continue;
+        CUDA_TRY(c, cudaMemcpyAsync(c->peer_x[q] + off, c->x + off, size_t(sh) * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    // ... and the peers must see every shard before their next read of x: node barrier
+    // (a virtual cluster's ranks share one stream, which already orders them)
+    if (!c->vc)
+        NCCL_TRY(c, ncclAllReduce(c->sig + 2 * c->G + 1, c->sig + 2 * c->G + 1, 1, ncclUint64, ncclSum,
+                                  c->node_comm, s));
+    return DASO_OK;
+}
+
+daso_status finish_blocking(daso_ctx* c, cudaStream_t s) {   // virtual cluster, after the loopback exchange
+    c->vc_blocking = false;
+    if (c->cfg.mode == DASO_MODE_FAITHFUL) return faithful_blocking_tail(c, c->vc_group, s);
+    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1) return fused_blocking_tail(c, s);
+    return shard_blocking_tail(c, s);
 }
 
 // ---- faithful (v1) batch ---------------------------------------------------------
@@ -268,13 +331,12 @@ daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStrea
     if (send) {
         if (send_here) STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {   // Fig. 3 average + Fig. 4 broadcast on the critical path
-            if (send_here) {
-                STATUS_TRY(wait_exchange(c, s));
-                daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
-                av.den = float(c->P);
-                KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+            if (c->vc) {
+                c->vc_blocking = true;
+                c->vc_group = int(r.send_group);
+                return DASO_OK;
             }
-            STATUS_TRY(node_bcast(c, int(r.send_group), s));
+            STATUS_TRY(faithful_blocking_tail(c, int(r.send_group), s));
         } else {
             c->inflight = true;
             c->infl_group = int(r.send_group);
@@ -314,10 +376,11 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
     if (send) {
         STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {
-            STATUS_TRY(wait_exchange(c, s));
-            daso::KernelArgs av = base_args(c, off, sh, 0.f);
-            av.den = float(c->P);
-            KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+            if (c->vc) {   // G == 1 in a virtual cluster: nothing follows the tail
+                c->vc_blocking = true;
+                return DASO_OK;
+            }
+            STATUS_TRY(shard_blocking_tail(c, s));
         } else {
             c->inflight = true;
             c->infl_group = int(r.send_group);
@@ -361,6 +424,18 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
     pa.done = reinterpret_cast<unsigned*>(c->sig + 2 * c->G);
     pa.err = c->d_flag;
     pa.epoch = ++c->epoch;
+    if (c->vc) {
+        // Virtual cluster: the node's G kernels run one after another on one stream, so no
+        // launch may wait for a later one (B200 guide: never launch kernels that wait on each
+        // other on one GPU).  The first rank of the node pre-sets every start and end signal
+        // of the node to this epoch, so every barrier wait is satisfied at its first poll;
+        // the kernels' own signal stores write the same values.  Stream order provides what
+        // the barriers provide across GPUs (all g complete before any read; all x stores
+        // complete before the next batch), and shards are disjoint, so the sequential
+        // execution computes exactly what G concurrent GPUs compute.
+        if (c->local == 0) KERN_TRY(c, daso::launch_fill_u64(c->vc_node_sig, c->G, 2 * c->G + 2, 2 * c->G, pa.epoch, s));
+        pa.timeout_ns = 1000ull * 1000 * 1000;
+    }
     pa.G = c->G;
     pa.me = c->local;
     {
@@ -386,18 +461,11 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
     if (send) {
         STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {
-            STATUS_TRY(wait_exchange(c, s));
-            // blocking average on the shard, then re-publish it to the node peers
-            daso::KernelArgs av = base_args(c, off, sh, 0.f);
-            av.den = float(c->P);
-            KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
-            for (int q = 0; q < c->G; ++q) {
-                if (q == c->local) continue;
-                CUDA_TRY(c, cudaMemcpyAsync(c->peer_x[q] + off, c->x + off, size_t(sh) * 4, cudaMemcpyDeviceToDevice, s));
+            if (c->vc) {
+                c->vc_blocking = true;
+                return DASO_OK;
             }
-            // the peers must see every shard before their next read of x: node barrier
-            NCCL_TRY(c, ncclAllReduce(c->sig + 2 * c->G + 1, c->sig + 2 * c->G + 1, 1, ncclUint64, ncclSum,
-                                      c->node_comm, s));
+            STATUS_TRY(fused_blocking_tail(c, s));
         } else {
             c->inflight = true;
             c->infl_group = int(r.send_group);
@@ -442,7 +510,12 @@ daso_status setup_peers(daso_ctx* c, bool sig_only) {
         size_t size = 0;
         if (range(&base, &size, CUdeviceptr(bufs[b])) != CUDA_SUCCESS)
             return c->fail(DASO_ERR_ARGUMENT, "buffer %d is not a device allocation", b);
-        CUDA_TRY(c, cudaIpcGetMemHandle(&mine.h[b], reinterpret_cast<void*>(base)));
+        const cudaError_t e = cudaIpcGetMemHandle(&mine.h[b], reinterpret_cast<void*>(base));
+        if (e != cudaSuccess)
+            return c->fail(DASO_ERR_ARGUMENT,
+                           "buffer %d cannot be exported by CUDA IPC (%s): the fused mode needs cudaMalloc-backed "
+                           "buckets (not cuMem / expandable_segments memory); use daso_alloc_bind",
+                           b, cudaGetErrorString(e));
         mine.base[b] = uint64_t(base);
         mine.off[b] = uint64_t(CUdeviceptr(bufs[b]) - base);
     }
@@ -513,9 +586,13 @@ daso_status daso_get_unique_id(void* out128) {
     return DASO_OK;
 }
 
-daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S, const daso_config* cfg,
-                      const void* uid) {
-    if (!out || !cfg || !uid) return DASO_ERR_ARGUMENT;
+}  // extern "C"
+
+namespace {
+
+// Validate the configuration and create a ctx with its streams, events and flag word, but
+// no communicators (daso_init adds them; a virtual cluster's ranks have none).
+daso_status make_ctx(daso_ctx** out, int world, int gpus_per_node, int B, int S, const daso_config* cfg) {
     *out = nullptr;
     if (world < 1 || gpus_per_node < 1 || world % gpus_per_node != 0 || B < 1) return DASO_ERR_CONFIG;
     if (cfg->rank < 0 || cfg->rank >= world) return DASO_ERR_RANGE;
@@ -550,6 +627,25 @@ daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S
     *out = c;   // returned even on failure so daso_last_error can be read
 
     CUDA_TRY(c, cudaGetDevice(&c->device));
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_exchanged, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaMalloc(&c->d_flag, sizeof(uint32_t)));
+    CUDA_TRY(c, cudaMemset(c->d_flag, 0, sizeof(uint32_t)));
+    return DASO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S, const daso_config* cfg,
+                      const void* uid) {
+    if (!out || !cfg || !uid) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(make_ctx(out, world, gpus_per_node, B, S, cfg));
+    daso_ctx* c = *out;
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof id);
     ncclConfig_t wc = NCCL_CONFIG_INITIALIZER;
@@ -568,14 +664,6 @@ daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S
     ncclConfig_t bc = NCCL_CONFIG_INITIALIZER;
     bc.blocking = 1;
     NCCL_TRY(c, ncclCommSplit(c->world_comm, c->node, c->local, &c->bucket_comm, &bc));
-
-    int lo = 0, hi = 0;
-    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_packed, cudaEventDisableTiming));
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_exchanged, cudaEventDisableTiming));
-    CUDA_TRY(c, cudaMalloc(&c->d_flag, sizeof(uint32_t)));
-    CUDA_TRY(c, cudaMemset(c->d_flag, 0, sizeof(uint32_t)));
     return DASO_OK;
 }
 
@@ -593,20 +681,26 @@ daso_status daso_alloc_bind(daso_ctx* c, size_t n, float** x, float** g, float**
     if (c->bound) return c->fail(DASO_ERR_PROTOCOL, "daso_bind called twice");
     const size_t n_pad = daso_padded_numel(n, c->G);
     const size_t bytes = (n_pad * sizeof(float) + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
-    void *px = nullptr, *pg = nullptr, *pv = nullptr;
-    NCCL_TRY(c, ncclMemAlloc(&px, bytes));
-    NCCL_TRY(c, ncclMemAlloc(&pg, bytes));
-    CUDA_TRY(c, cudaMalloc(&pv, bytes));
-    c->owns_buckets = true;
-    c->x = static_cast<float*>(px);
-    c->g = static_cast<float*>(pg);
-    c->v = static_cast<float*>(pv);
-    CUDA_TRY(c, cudaMemset(px, 0, bytes));
-    CUDA_TRY(c, cudaMemset(pg, 0, bytes));
-    CUDA_TRY(c, cudaMemset(pv, 0, bytes));
-    if (c->cfg.mode == DASO_MODE_NVLS && c->G > 1) {
+    // NVLS needs NCCL symmetric memory (ncclMemAlloc: cuMem-backed, multicast-capable); every
+    // other mode gets plain cudaMalloc, which the fused mode's CUDA IPC export requires.
+    const bool sym = c->cfg.mode == DASO_MODE_NVLS && c->G > 1;
+    void* p[3] = {nullptr, nullptr, nullptr};
+    for (int b = 0; b < 3; ++b) {
+        if (sym && b < 2) {
+            NCCL_TRY(c, ncclMemAlloc(&p[b], bytes));
+            c->own_nccl[b] = p[b];
+        } else {
+            CUDA_TRY(c, cudaMalloc(&p[b], bytes));
+            c->own_cuda[b] = p[b];
+        }
+        CUDA_TRY(c, cudaMemset(p[b], 0, bytes));
+    }
+    c->x = static_cast<float*>(p[0]);
+    c->g = static_cast<float*>(p[1]);
+    c->v = static_cast<float*>(p[2]);
+    if (sym) {
         const char* why = nullptr;
-        const int r = daso::nvls_setup(c->node_comm, px, pg, bytes, c->G, &c->nvls, &why);
+        const int r = daso::nvls_setup(c->node_comm, p[0], p[1], bytes, c->G, &c->nvls, &why);
         if (r == 1) return c->fail(DASO_ERR_NCCL, "NVLS setup: %s", why);
         if (r == 2) return c->fail(DASO_ERR_CONFIG, "NVLS setup: %s", why);
         if (r == 3) return c->fail(DASO_ERR_CUDA, "NVLS setup: %s", why);
@@ -641,7 +735,7 @@ daso_status bind_impl(daso_ctx* c, float* x, float* g, float* v, size_t n) {
         CUDA_TRY(c, cudaMalloc(&c->slot, bytes));
         CUDA_TRY(c, cudaMemset(c->slot, 0, bytes));
     }
-    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1) STATUS_TRY(setup_peers(c, false));
+    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1 && !c->vc) STATUS_TRY(setup_peers(c, false));
     if (c->cfg.mode == DASO_MODE_NVLS && c->G > 1) STATUS_TRY(setup_peers(c, true));
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->bound = true;
@@ -811,7 +905,8 @@ daso_status daso_check_finite(daso_ctx* c, void* stream) {
     CUDA_TRY(c, cudaMemsetAsync(c->d_flag, 0, sizeof(uint32_t), s));
     CUDA_TRY(c, cudaStreamSynchronize(s));
     if (h & 2u) return c->fail(DASO_ERR_PROTOCOL, "node barrier timed out in the fused kernel (a peer never arrived)");
-    if (h) return c->fail(DASO_ERR_NONFINITE, "non-finite parameter written");
+    if (h & 4u) return c->fail(DASO_ERR_CUDA, "a TMA bulk-copy wait timed out (transfer never completed)");
+    if (h & 1u) return c->fail(DASO_ERR_NONFINITE, "non-finite parameter written");
     return DASO_OK;
 }
 
@@ -821,6 +916,41 @@ daso_status daso_topology(const daso_ctx* c, int* P, int* G, int* node, int* loc
     if (G) *G = c->G;
     if (node) *node = c->node;
     if (local) *local = c->local;
+    return DASO_OK;
+}
+
+int daso_set_exchange(daso_ctx* c, int enabled) {
+    if (!c) return -1;
+    const int prev = c->exch_enabled ? 1 : 0;
+    if (enabled == 0 || enabled == 1) c->exch_enabled = enabled == 1;
+    return prev;
+}
+
+daso_status daso_exchange_alone(daso_ctx* c, int iters, double* ms_out) {
+    if (!c || !ms_out || iters < 1) return DASO_ERR_ARGUMENT;
+    STATUS_TRY(require_bound(c));
+    if (c->vc) return c->fail(DASO_ERR_PROTOCOL, "no group communicator in a virtual cluster");
+    if (c->P == 1) {
+        *ms_out = 0.0;
+        return DASO_OK;
+    }
+    if (c->inflight) return c->fail(DASO_ERR_PROTOCOL, "an exchange is in flight");
+    CUDA_TRY(c, cudaDeviceSynchronize());
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CUDA_TRY(c, cudaEventCreate(&e0));
+    CUDA_TRY(c, cudaEventCreate(&e1));
+    NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm, c->side));
+    CUDA_TRY(c, cudaEventRecord(e0, c->side));
+    for (int i = 0; i < iters; ++i)
+        NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
+                                  c->side));
+    CUDA_TRY(c, cudaEventRecord(e1, c->side));
+    CUDA_TRY(c, cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_TRY(c, cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = double(ms) / iters;
     return DASO_OK;
 }
 
@@ -839,11 +969,10 @@ daso_status daso_finalize(daso_ctx* c) {
         if (c->sig) cudaFree(c->sig);
     }
     daso::nvls_teardown(c->node_comm, &c->nvls);
-    if (c->owns_buckets) {
-        cudaDeviceSynchronize();
-        if (c->x) ncclMemFree(c->x);
-        if (c->g) ncclMemFree(c->g);
-        if (c->v) cudaFree(c->v);
+    cudaDeviceSynchronize();
+    for (int b = 0; b < 3; ++b) {
+        if (c->own_nccl[b]) ncclMemFree(c->own_nccl[b]);
+        if (c->own_cuda[b]) cudaFree(c->own_cuda[b]);
     }
     ncclComm_t comms[4] = {c->bucket_comm, c->group_comm, c->node_comm, c->world_comm};
     for (ncclComm_t m : comms) {
@@ -863,6 +992,157 @@ daso_status daso_finalize(daso_ctx* c) {
 }
 
 const char* daso_last_error(const daso_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+// ---------------------------------------------------------------- virtual cluster (one GPU)
+// W = P x G virtual ranks, each a full daso_ctx running the product step path (daso_step_ex
+// -> step_fused / step_sharded / step_faithful -> the same kernels), on one device and one
+// stream.  Only the transport differs: the node tier's peers are the sibling ranks' buffers
+// on the same GPU (the fused kernel's barriers are pre-satisfied, see step_fused), and the
+// group all-gather (a4) is a device-to-device copy of every packed row into every group
+// member's slot, issued after all ranks ran their batch.  This lets the multi-rank path be
+// parity-tested against the oracle at any topology on a one-GPU box.
+struct daso_vcluster {
+    int world = 0, G = 0, P = 0;
+    std::vector<daso_ctx*> rank;
+    std::vector<void*> owned;   // device allocations (buckets, signal blocks)
+    std::string err;
+    daso_status fail(daso_status s, const std::string& m) {
+        err = m;
+        return s;
+    }
+};
+
+daso_status daso_vcluster_create(daso_vcluster** out, int world, int gpus_per_node, int B, int S,
+                                 const daso_config* cfg, size_t n) {
+    if (!out || !cfg || n == 0) return DASO_ERR_ARGUMENT;
+    *out = nullptr;
+    const bool fused = cfg->mode == DASO_MODE_FUSED;
+    if (!fused && gpus_per_node != 1) return DASO_ERR_CONFIG;   // NCCL node collectives cannot loop back
+    if (cfg->mode == DASO_MODE_NVLS) return DASO_ERR_CONFIG;
+    daso_vcluster* v = new (std::nothrow) daso_vcluster;
+    if (!v) return DASO_ERR_ARGUMENT;
+    *out = v;
+    v->world = world;
+    v->G = gpus_per_node;
+    v->P = gpus_per_node > 0 ? world / gpus_per_node : 0;
+    for (int r = 0; r < world; ++r) {
+        daso_config rc = *cfg;
+        rc.rank = r;
+        daso_ctx* c = nullptr;
+        const daso_status st = make_ctx(&c, world, gpus_per_node, B, S, &rc);
+        if (c) v->rank.push_back(c);
+        if (st != DASO_OK) return v->fail(st, c ? c->err : "invalid virtual-cluster configuration");
+        c->vc = v;
+    }
+    const size_t n_pad = daso_padded_numel(n, gpus_per_node);
+    for (daso_ctx* c : v->rank) {
+        void* p[3] = {nullptr, nullptr, nullptr};
+        for (int b = 0; b < 3; ++b) {
+            if (cudaMalloc(&p[b], n_pad * sizeof(float)) != cudaSuccess ||
+                cudaMemset(p[b], 0, n_pad * sizeof(float)) != cudaSuccess)
+                return v->fail(DASO_ERR_CUDA, "virtual cluster: bucket allocation failed");
+            v->owned.push_back(p[b]);
+        }
+        const daso_status st = bind_impl(c, static_cast<float*>(p[0]), static_cast<float*>(p[1]),
+                                         static_cast<float*>(p[2]), n);
+        if (st != DASO_OK) return v->fail(st, c->err);
+    }
+    if (fused && gpus_per_node > 1) {   // node tier over the siblings' buffers + one signal block per node
+        const int G = gpus_per_node, row = 2 * G + 2;
+        for (int j = 0; j < v->P; ++j) {
+            void* blk = nullptr;
+            if (cudaMalloc(&blk, size_t(G) * row * sizeof(unsigned long long)) != cudaSuccess ||
+                cudaMemset(blk, 0, size_t(G) * row * sizeof(unsigned long long)) != cudaSuccess)
+                return v->fail(DASO_ERR_CUDA, "virtual cluster: signal allocation failed");
+            v->owned.push_back(blk);
+            auto* sig = static_cast<unsigned long long*>(blk);
+            for (int l = 0; l < G; ++l) {
+                daso_ctx* c = v->rank[size_t(j) * G + l];
+                c->sig = sig + size_t(l) * row;
+                c->vc_node_sig = sig;
+                for (int q = 0; q < G; ++q) {
+                    daso_ctx* peer = v->rank[size_t(j) * G + q];
+                    c->peer_x[q] = peer->x;
+                    c->peer_g[q] = peer->g;
+                    c->peer_sig[q] = sig + size_t(q) * row;
+                }
+            }
+        }
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return v->fail(DASO_ERR_CUDA, "virtual cluster: setup failed");
+    return DASO_OK;
+}
+
+daso_status daso_vcluster_buffers(daso_vcluster* v, int rank, float** x, float** g, float** vb) {
+    if (!v || rank < 0 || rank >= int(v->rank.size())) return DASO_ERR_RANGE;
+    daso_ctx* c = v->rank[size_t(rank)];
+    if (x) *x = c->x;
+    if (g) *g = c->g;
+    if (vb) *vb = c->v;
+    return DASO_OK;
+}
+
+daso_ctx* daso_vcluster_rank(daso_vcluster* v, int rank) {
+    if (!v || rank < 0 || rank >= int(v->rank.size())) return nullptr;
+    return v->rank[size_t(rank)];
+}
+
+daso_status daso_vcluster_step(daso_vcluster* v, float lr, int plateau, void* stream, daso_record* out) {
+    if (!v || v->rank.empty()) return DASO_ERR_ARGUMENT;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    daso_record r0{};
+    bool sent = false, blocking = false;
+    for (size_t i = 0; i < v->rank.size(); ++i) {   // every rank's batch, in rank order
+        daso_ctx* c = v->rank[i];
+        c->vc_sent = c->vc_blocking = false;
+        daso_record r{};
+        const daso_status st = daso_step_ex(c, lr, plateau, 0, stream, &r);
+        if (st != DASO_OK) return v->fail(st, "rank " + std::to_string(i) + ": " + c->err);
+        if (i == 0) r0 = r;
+        else if (std::memcmp(&r, &r0, sizeof r) != 0) return v->fail(DASO_ERR_PROTOCOL, "ranks disagree on the schedule");
+        if (out) out[i] = r;
+        sent |= c->vc_sent;
+        blocking |= c->vc_blocking;
+    }
+    if (sent) {   // loopback group all-gather: member (i, l)'s packed row -> row i of every member (j, l)
+        const size_t wb = v->rank[0]->wire_bytes, seg = size_t(v->rank[0]->seg);
+        for (int l = 0; l < v->G; ++l)
+            for (int i = 0; i < v->P; ++i) {
+                daso_ctx* src = v->rank[size_t(i) * v->G + l];
+                if (!src->vc_sent) continue;
+                for (int j = 0; j < v->P; ++j) {
+                    if (j == i) continue;
+                    daso_ctx* dst = v->rank[size_t(j) * v->G + l];
+                    if (cudaMemcpyAsync(static_cast<char*>(dst->slot) + size_t(i) * seg * wb, own_segment(src),
+                                        seg * wb, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                        return v->fail(DASO_ERR_CUDA, "virtual cluster: loopback all-gather copy failed");
+                }
+            }
+    }
+    if (blocking)
+        for (size_t i = 0; i < v->rank.size(); ++i) {
+            daso_ctx* c = v->rank[i];
+            if (!c->vc_blocking) continue;
+            const daso_status st = finish_blocking(c, s);
+            if (st != DASO_OK) return v->fail(st, "rank " + std::to_string(i) + ": " + c->err);
+        }
+    return DASO_OK;
+}
+
+daso_status daso_vcluster_destroy(daso_vcluster* v) {
+    if (!v) return DASO_OK;
+    cudaDeviceSynchronize();
+    daso_status st = DASO_OK;
+    for (daso_ctx* c : v->rank) {
+        c->sig = nullptr;   // owned by the cluster's signal blocks
+        if (daso_finalize(c) != DASO_OK) st = DASO_ERR_CUDA;
+    }
+    for (void* p : v->owned) cudaFree(p);
+    delete v;
+    return st;
+}
+
+const char* daso_vcluster_last_error(const daso_vcluster* v) { return v ? v->err.c_str() : "null cluster"; }
 
 // ---------------------------------------------------------------- kernel entry points
 static bool aligned16(const void* p) { return (uintptr_t(p) & 15u) == 0; }

@@ -46,7 +46,8 @@ struct KernelArgs {
     int P = 0;
     float den = 1.f;              // 2S + P (merge) or P (average)
     void* pack_out = nullptr;
-    uint32_t* flag = nullptr;
+    uint32_t* flag = nullptr;     // bit 0: non-finite parameter (nullable: check off)
+    uint32_t* err = nullptr;      // bit 2: TMA (mbarrier) wait timed out (nullable)
 };
 
 int launch_fused(int ops, int wire, const KernelArgs& a, void* stream);
@@ -64,6 +65,7 @@ struct PeerArgs {
     float* x_mc = nullptr;                     // NVLS: multicast address of x at this shard
     const float* g_mc = nullptr;               // NVLS: multicast address of g at this shard
     unsigned long long epoch = 0;              // monotonically increasing barrier value
+    unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;   // barrier wait limit (then bit 1 of err)
     int G = 1, me = 0;
 };
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream);
@@ -89,5 +91,8 @@ int launch_gather(const float* const* src, const size_t* numel, const size_t* of
 int launch_scatter(const float* src, float* const* dst, const size_t* numel, const size_t* offsets,
                    int count, void* stream);
 int launch_checksum(const float* x, int64_t n, uint64_t* out, void* stream);
+// Set base[r * row_stride + c] = value for r < rows, c < cols (virtual-cluster barrier pre-set).
+int launch_fill_u64(unsigned long long* base, int rows, int row_stride, int cols, unsigned long long value,
+                    void* stream);
 
 }  // namespace daso

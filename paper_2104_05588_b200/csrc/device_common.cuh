@@ -148,16 +148,18 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 // Wait for an mbarrier phase.  A transfer that never completes (a bug, a dead peer
-// mapping) must not hang the GPU: after 20 s give up and raise bit 2 of *err.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t* err = nullptr) {
-    if (mbar_try_wait(bar, parity)) return;
+// mapping) must not hang the GPU: after 20 s give up, raise bit 2 of *err and return
+// false (the caller stops using the stage: its data never arrived).
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, uint32_t* err = nullptr) {
+    if (mbar_try_wait(bar, parity)) return true;
     const unsigned long long t0 = globaltimer_ns();
     while (!mbar_try_wait(bar, parity)) {
         if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) {
             if (err) atomicOr(err, 4u);
-            return;
+            return false;
         }
     }
+    return true;
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(

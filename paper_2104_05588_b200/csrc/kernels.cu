@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_kernel(const KernelArgs a,
     for (int64_t k = 0; k < my; ++k) {
         const int s = int(k % NS);
         unsigned char* st = smem + size_t(s) * L.bytes;
-        mbar_wait(&full[s], uint32_t((k / NS) & 1), a.flag);
+        if (!mbar_wait(&full[s], uint32_t((k / NS) & 1), a.err)) break;   // timed out: bit 2 raised, stop
         const int i = threadIdx.x * kVec;
         float* xs = reinterpret_cast<float*>(st + L.x) + i;
         float* vs = reinterpret_cast<float*>(st + L.v) + i;
@@ -284,10 +284,12 @@ int launch_tma(const KernelArgs& a, cudaStream_t s) {
     int NS = int(std::min<int64_t>(8, (budget - 64) / L.bytes));
     if (NS < 2) return launch_t<OPS, WIRE>(a, s);
     const size_t smem = size_t(NS) * L.bytes + 8 * size_t(NS);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(tma_kernel<OPS, WIRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+    static size_t attr = 0;   // opt-in limit set so far
+    if (smem > attr) {
+        const cudaError_t e = cudaFuncSetAttribute(tma_kernel<OPS, WIRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   int(smem));
+        if (e != cudaSuccess) return int(e);
+        attr = smem;
     }
     tma_kernel<OPS, WIRE><<<dim3(unsigned(sm_count())), dim3(kTmaThreads), smem, s>>>(a, NS);
     return int(cudaGetLastError());
@@ -388,7 +390,17 @@ __global__ void __launch_bounds__(kThreads) checksum_kernel(const uint32_t* __re
     }
 }
 
+__global__ void fill_u64_kernel(unsigned long long* base, int rows, int row_stride, int cols, unsigned long long v) {
+    for (int k = threadIdx.x; k < rows * cols; k += blockDim.x) base[(k / cols) * row_stride + k % cols] = v;
+}
+
 }  // namespace
+
+int launch_fill_u64(unsigned long long* base, int rows, int row_stride, int cols, unsigned long long value,
+                    void* stream) {
+    fill_u64_kernel<<<1, 128, 0, static_cast<cudaStream_t>(stream)>>>(base, rows, row_stride, cols, value);
+    return int(cudaGetLastError());
+}
 
 int current_kernel_impl() { return kernel_impl(); }
 

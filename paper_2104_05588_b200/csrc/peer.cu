@@ -42,19 +42,56 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 
 // Spin until *p >= v.  A peer that never arrives (crashed process, protocol bug) must not
-// hang the GPU: after kBarrierTimeoutNs the wait gives up and raises bit 1 of the flag,
-// which daso_check_finite / the next step report as an error.
-constexpr unsigned long long kBarrierTimeoutNs = 20ull * 1000 * 1000 * 1000;
-
-__device__ __forceinline__ void wait_geq(const unsigned long long* p, unsigned long long v, uint32_t* flag) {
-    if (ld_acquire_sys(p) >= v) return;
+// hang the GPU: after `timeout_ns` the wait gives up, raises bit 1 of the error word
+// (daso_check_finite reports it) and returns false; the kernel then skips its body, so
+// it never reads or writes unsynchronised peer memory.
+__device__ __forceinline__ bool wait_geq(const unsigned long long* p, unsigned long long v, uint32_t* flag,
+                                         unsigned long long timeout_ns) {
+    if (ld_acquire_sys(p) >= v) return true;
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys(p) < v) {
-        if (globaltimer_ns() - t0 > kBarrierTimeoutNs) {
+        if (globaltimer_ns() - t0 > timeout_ns) {
             if (flag) atomicOr(flag, 2u);
-            return;
+            return false;
         }
         __nanosleep(64);
+    }
+    return true;
+}
+
+// Start barrier: CTA 0 signals every node peer "my g is ready" (slot `me` of their
+// start row); thread 0 of every CTA waits for all G start signals.  Returns false (in
+// every thread of the CTA) if a wait timed out.
+__device__ __forceinline__ bool start_barrier(const PeerArgs& pa, int G) {
+    __shared__ int s_ok;
+    if (blockIdx.x == 0 && threadIdx.x < G) {
+        __threadfence_system();
+        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
+    }
+    if (threadIdx.x == 0) {
+        bool ok = true;
+        for (int q = 0; q < G && ok; ++q) ok = wait_geq(pa.sig_me + q, pa.epoch, pa.err, pa.timeout_ns);
+        s_ok = ok;
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// End barrier: the last CTA to finish (CTA counter `done`) signals every peer "my x
+// stores and g reads are complete" after a system fence and waits for all peers, so when
+// the kernel completes the node holds the full new x and no peer still reads this g.
+__device__ __forceinline__ void end_barrier(const PeerArgs& pa, int G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned prev = atomicAdd(pa.done, 1u);
+        if (prev == gridDim.x - 1) {
+            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
+            __threadfence_system();
+            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
+            for (int q = 0; q < G; ++q)
+                if (!wait_geq(pa.sig_me + G + q, pa.epoch, pa.err, pa.timeout_ns)) break;
+        }
     }
 }
 
@@ -104,14 +141,7 @@ __device__ __forceinline__ void peer_body(const PeerArgs& pa, int64_t i, bool& b
 
 template <int OPS, int WIRE, int G>
 __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
-    // 1. start barrier
-    if (blockIdx.x == 0 && threadIdx.x < G) {
-        __threadfence_system();
-        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
-    }
-    if (threadIdx.x == 0)
-        for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + q, pa.epoch, pa.err);
-    __syncthreads();
+    if (!start_barrier(pa, G)) return;   // 1. start barrier (timed out: error bit raised, do nothing)
     // 2. shard update over NVLink
     bool bad = false;
     const int64_t n = pa.a.n;
@@ -127,18 +157,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
         if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
     }
-    // 3. end barrier
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(pa.done, 1u);
-        if (prev == gridDim.x - 1) {
-            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
-            __threadfence_system();
-            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
-            for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + G + q, pa.epoch, pa.err);
-        }
-    }
+    end_barrier(pa, G);   // 3. end barrier
 }
 
 int peer_blocks_per_sm() {   // grid = SMs x this (DASO_PEER_BPSM, default 2 (measured best)); one-shot if larger
@@ -202,13 +221,8 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     unsigned char* outs = smem + size_t(NS) * L.in_bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(kPeerOut) * L.out_bytes);
     const bool leader = threadIdx.x == 0;
-    // 1. start barrier
-    if (blockIdx.x == 0 && threadIdx.x < G) {
-        __threadfence_system();
-        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
-    }
+    if (!start_barrier(pa, G)) return;   // 1. start barrier (timed out: error bit raised, do nothing)
     if (leader) {
-        for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + q, pa.epoch, pa.err);
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async_global();
@@ -243,7 +257,7 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
         unsigned char* st = smem + size_t(s) * L.in_bytes;
         unsigned char* ob = outs + size_t(k % kPeerOut) * L.out_bytes;
         if (leader && k >= kPeerOut) bulk_wait_read<kPeerOut - 1>();   // output buffer ob drained
-        mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err);
+        if (!mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err)) break;   // timed out: bit 2 raised, stop
         __syncthreads();                                                 // also publishes the drain
         const int i = threadIdx.x * 8;
         float x[8], v[8], g[8];
@@ -305,18 +319,8 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
         if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
     }
     // 3. end barrier (all bulk stores of this CTA are complete: wait_group 0 above)
-    __syncthreads();
-    if (leader) {
-        fence_proxy_async_global();
-        __threadfence_system();
-        const unsigned prev = atomicAdd(pa.done, 1u);
-        if (prev == gridDim.x - 1) {
-            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
-            __threadfence_system();
-            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
-            for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + G + q, pa.epoch, pa.err);
-        }
-    }
+    if (leader) fence_proxy_async_global();
+    end_barrier(pa, G);
 }
 
 template <int OPS, int WIRE, int G>
@@ -326,12 +330,14 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     const int budget = 210 * 1024 - kPeerOut * int(L.out_bytes);
     const int NS = int(std::min<int64_t>(8, (budget - 64) / L.in_bytes));
     if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
     const size_t smem = size_t(NS) * L.in_bytes + size_t(kPeerOut) * L.out_bytes + 8 * size_t(NS);
+    static size_t attr = 0;   // opt-in limit set so far (static + dynamic must fit the 227 KB per CTA)
+    if (smem > attr) {
+        const cudaError_t e = cudaFuncSetAttribute(peer_tma_kernel<OPS, WIRE, G>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return int(e);
+        attr = smem;
+    }
     // DASO_PEER_TMA_CTAS: persistent CTAs.  Default: one per SM minus 16, so the side-stream
     // exchange's NCCL kernels always find free SMs (2x2: exchange hidden 0.98 vs 0.73 with every
     // SM taken, same kernel time; profiles/r01/b20_*).
@@ -512,13 +518,7 @@ int nvls_ctas() {
 template <int OPS, int WIRE>
 __global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
     const int G = pa.G;
-    if (blockIdx.x == 0 && threadIdx.x < G) {   // 1. start barrier: every peer's g is complete
-        __threadfence_system();
-        st_release_sys(pa.sig_peer[threadIdx.x] + pa.me, pa.epoch);
-    }
-    if (threadIdx.x == 0)
-        for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + q, pa.epoch, pa.err);
-    __syncthreads();
+    if (!start_barrier(pa, G)) return;           // 1. start barrier: every peer's g is complete
     bool bad = false;
     const int64_t n = pa.a.n;
     const int64_t nch = n / kNV;
@@ -532,17 +532,7 @@ __global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
         if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
     }
-    __syncthreads();                             // 3. end barrier: every peer's shard has landed
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned prev = atomicAdd(pa.done, 1u);
-        if (prev == gridDim.x - 1) {
-            *reinterpret_cast<volatile unsigned*>(pa.done) = 0u;
-            __threadfence_system();
-            for (int q = 0; q < G; ++q) st_release_sys(pa.sig_peer[q] + G + pa.me, pa.epoch);
-            for (int q = 0; q < G; ++q) wait_geq(pa.sig_me + G + q, pa.epoch, pa.err);
-        }
-    }
+    end_barrier(pa, G);                          // 3. end barrier: every peer's shard has landed
 }
 
 template <int OPS, int WIRE>

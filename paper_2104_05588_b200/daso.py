@@ -116,8 +116,10 @@ def rendezvous_unique_id() -> bytes:
 class Ctx:
     """An initialised ``daso_ctx*``; methods are the ctx entry points of daso.h."""
 
-    def __init__(self, handle: C.c_void_p, world: int, gpus_per_node: int, rank: int, mode: str, wire: str):
+    def __init__(self, handle: C.c_void_p, world: int, gpus_per_node: int, rank: int, mode: str, wire: str,
+                 owned: bool = True):
         self._h = handle
+        self._owned = owned
         self.world, self.G, self.rank = world, gpus_per_node, rank
         self.P = world // gpus_per_node
         self.node, self.local = rank // gpus_per_node, rank % gpus_per_node
@@ -148,14 +150,8 @@ class Ctx:
         self._check(lib().daso_alloc_bind(self._h, int(n), C.byref(px), C.byref(pg), C.byref(pv)), "daso_alloc_bind")
         self.n = int(n)
         n_pad = daso_padded_numel(n, self.G)
-
-        class _Buf:
-            def __init__(self, ptr, owner):
-                self._owner = owner
-                self.__cuda_array_interface__ = {"shape": (n_pad,), "typestr": "<f4", "data": (int(ptr), False),
-                                                 "version": 3, "strides": None}
         dev = torch.device("cuda", torch.cuda.current_device())
-        return tuple(torch.as_tensor(_Buf(p.value, self), device=dev) for p in (px, pg, pv))
+        return tuple(torch.as_tensor(_DevBuf(p.value, n_pad, self), device=dev) for p in (px, pg, pv))
 
     def local_sync(self, stream=None):
         self._check(lib().daso_local_sync(self._h, _stream(stream)), "daso_local_sync")
@@ -203,6 +199,16 @@ class Ctx:
         self._check(lib().daso_trace_read(self._h, C.byref(t), int(reset)), "daso_trace_read")
         return t.as_dict()
 
+    def set_exchange(self, enabled: bool) -> bool:
+        """Timing knob (daso_set_exchange): False suppresses the group all-gather."""
+        return bool(lib().daso_set_exchange(self._h, int(bool(enabled))))
+
+    def exchange_alone(self, iters: int = 20) -> float:
+        """daso_exchange_alone: mean ms of one group all-gather with nothing else running."""
+        ms = C.c_double()
+        self._check(lib().daso_exchange_alone(self._h, int(iters), C.byref(ms)), "daso_exchange_alone")
+        return float(ms.value)
+
     def query(self) -> dict:
         r = Record()
         self._check(lib().daso_query(self._h, C.byref(r)), "daso_query")
@@ -216,6 +222,8 @@ class Ctx:
         return True
 
     def finalize(self):
+        if not self._owned:
+            raise RuntimeError("a virtual-cluster rank is finalized by VCluster.destroy()")
         if self._h:
             s = lib().daso_finalize(self._h)
             self._h = None
@@ -227,8 +235,8 @@ def daso_init(world: int, gpus_per_node: int, B: int, S: int, *, rank: int, uid:
               steps_per_epoch: int = 1 << 20, momentum: float = 0.9, weight_decay: float = 1e-4,
               wire: str = "bf16", mode: str = "faithful", check_finite: bool = True,
               nccl_max_ctas: int = 0) -> Ctx:
-    cfg = L.Config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay,
-                   WIRES[wire], MODES[mode], int(check_finite), nccl_max_ctas)
+    cfg = _config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay, wire,
+                  mode, check_finite, nccl_max_ctas)
     if len(uid) != 128:
         raise ValueError("uid must be 128 bytes")
     h = C.c_void_p()
@@ -239,6 +247,84 @@ def daso_init(world: int, gpus_per_node: int, B: int, S: int, *, rank: int, uid:
             lib().daso_finalize(h)
         raise DasoError(s, "daso_init", msg)
     return Ctx(h, world, gpus_per_node, rank, mode, wire)
+
+
+def _config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay, wire, mode,
+            check_finite, nccl_max_ctas) -> L.Config:
+    return L.Config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay,
+                    WIRES[wire], MODES[mode], int(check_finite), nccl_max_ctas)
+
+
+class VCluster:
+    """daso_vcluster_*: W = world virtual ranks of a P x G cluster on ONE GPU, each running the
+    product batch (daso_step_ex and its kernels) with a loopback transport (include/daso.h).
+    ``x(r)``, ``g(r)``, ``v(r)`` are torch views of rank r's cluster-owned buckets
+    (daso_padded_numel(n, G) floats); ``rank(r)`` is its Ctx (trace / query / check_finite)."""
+
+    def __init__(self, world: int, gpus_per_node: int, B: int, S: int, n: int, *, warmup_epochs: int = 0,
+                 cooldown_epochs: int = 0, total_epochs: int = 1, steps_per_epoch: int = 1 << 20,
+                 momentum: float = 0.9, weight_decay: float = 1e-4, wire: str = "bf16", mode: str = "fused",
+                 check_finite: bool = True):
+        torch = _torch()
+        cfg = _config(0, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay,
+                      wire, mode, check_finite, 0)
+        h = C.c_void_p()
+        s = lib().daso_vcluster_create(C.byref(h), world, gpus_per_node, B, S, C.byref(cfg), int(n))
+        if s != L.OK:
+            msg = lib().daso_vcluster_last_error(h).decode() if h.value else ""
+            if h.value:
+                lib().daso_vcluster_destroy(h)
+            raise DasoError(s, "daso_vcluster_create", msg)
+        self._h = h
+        self.world, self.G, self.n = world, gpus_per_node, int(n)
+        self.P = world // gpus_per_node
+        self.n_pad = daso_padded_numel(n, gpus_per_node)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._bufs = []
+        for r in range(world):
+            px, pg, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
+            check(lib().daso_vcluster_buffers(h, r, C.byref(px), C.byref(pg), C.byref(pv)), "daso_vcluster_buffers")
+            self._bufs.append(tuple(torch.as_tensor(_DevBuf(p.value, self.n_pad, self), device=dev)
+                                    for p in (px, pg, pv)))
+        self._ranks = [Ctx(C.c_void_p(lib().daso_vcluster_rank(h, r)), world, gpus_per_node, r, mode, wire,
+                           owned=False) for r in range(world)]
+        for c in self._ranks:
+            c.n = self.n
+
+    def x(self, r: int):
+        return self._bufs[r][0]
+
+    def g(self, r: int):
+        return self._bufs[r][1]
+
+    def v(self, r: int):
+        return self._bufs[r][2]
+
+    def rank(self, r: int) -> Ctx:
+        return self._ranks[r]
+
+    def step(self, lr: float, plateau: int = 0, stream=None) -> list[dict]:
+        recs = (Record * self.world)()
+        s = lib().daso_vcluster_step(self._h, float(lr), int(plateau), _stream(stream), recs)
+        if s != L.OK:
+            raise DasoError(s, "daso_vcluster_step", lib().daso_vcluster_last_error(self._h).decode())
+        return [r.as_dict() for r in recs]
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            self._bufs = []
+            s = lib().daso_vcluster_destroy(self._h)
+            self._h = None
+            check(s, "daso_vcluster_destroy")
+
+
+class _DevBuf:
+    """__cuda_array_interface__ over library-owned device memory (kept alive by `owner`)."""
+
+    def __init__(self, ptr: int, numel: int, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
 
 
 def init_from_env(gpus_per_node: int, B: int, S: int, **kw) -> Ctx:

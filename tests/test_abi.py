@@ -139,3 +139,22 @@ def test_bucket_partition_tiles_the_bucket():
             assert all(offsets[i] >= off and offsets[i] + numels[i] <= off + cnt for i in b)
         assert pos == 0
         assert all(cnt >= limit for (_, cnt) in ranges[:-1]) or len(ranges) == 1
+
+
+@pytest.mark.parametrize("world,G,mode,expect", [
+    (4, 2, L.MODE_FAITHFUL, L.ERR_CONFIG),   # NCCL node collectives cannot loop back on one GPU
+    (4, 2, L.MODE_SHARDED, L.ERR_CONFIG),
+    (4, 2, L.MODE_NVLS, L.ERR_CONFIG),
+    (4, 3, L.MODE_FUSED, L.ERR_CONFIG),      # world % G != 0
+    (18, 9, L.MODE_FUSED, L.ERR_CONFIG),     # G > 8 peers
+])
+def test_vcluster_validation_before_any_device_work(world, G, mode, expect):
+    import ctypes as C
+    cfg = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, L.WIRE_BF16, mode, 1, 0)
+    h = C.c_void_p()
+    assert L.lib().daso_vcluster_create(C.byref(h), world, G, 4, 1, C.byref(cfg), 1000) == expect
+    if h.value:
+        L.lib().daso_vcluster_destroy(h)
+    assert L.lib().daso_vcluster_create(None, 2, 1, 4, 1, C.byref(cfg), 1000) == L.ERR_ARGUMENT
+    assert L.lib().daso_vcluster_rank(None, 0) is None
+    assert L.lib().daso_vcluster_destroy(None) == L.OK
