@@ -518,9 +518,12 @@ class FlatParams:
     "buffer packaging") and re-point every parameter and its ``.grad`` as views,
     so the per-step unpack is free.  Buckets x, g, v hold n_pad elements."""
 
-    def __init__(self, params, gpus_per_node: int = 1, align: int = 64, ctx: "Ctx | None" = None):
+    def __init__(self, params, gpus_per_node: int = 1, align: int = 64, ctx: "Ctx | None" = None,
+                 buckets=None):
         """ctx given: the buckets are allocated and bound by the library (daso_alloc_bind —
-        required for the "nvls" mode); otherwise torch allocates them and the caller binds."""
+        required for the "nvls" mode, and the fused mode's way around cuMem allocators);
+        buckets=(x, g, v) given: adopt existing (e.g. VCluster-owned) float32 buckets of
+        >= n_pad elements; otherwise torch allocates them and the caller binds."""
         torch = _torch()
         self.params = [p for p in params if p.requires_grad]
         if not self.params:
@@ -530,6 +533,12 @@ class FlatParams:
         self.n_pad = daso_padded_numel(self.n, gpus_per_node)
         if ctx is not None:
             self.x, self.g, self.v = ctx.alloc_bind(self.n)
+        elif buckets is not None:
+            for t, nm in zip(buckets, "xgv"):
+                _dev_f32(t, nm)
+                if t.numel() < self.n_pad:
+                    raise ValueError(f"bucket {nm} holds {t.numel()} < {self.n_pad} elements")
+            self.x, self.g, self.v = buckets
         else:
             self.x = torch.zeros(self.n_pad, dtype=torch.float32, device=dev)
             self.g = torch.zeros_like(self.x)

@@ -62,7 +62,7 @@ def HMSA(classes: int):
     return _HMSA()
 
 
-def train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank):
+def train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank, overlap=None):
     """The whole DASO control loop on real (synthetic-data) losses: per epoch, the mean training
     loss over all ranks feeds the plateau detector (daso_plateau_*); a plateau decays the
     LR (daso_lr_at) and is passed to the next epoch's first daso_step, which halves or
@@ -81,7 +81,8 @@ def train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank):
             with torch.autocast("cuda", dtype=torch.bfloat16):
                 loss = loss_fn(net(images), labels)
             loss.backward()
-            rec = ctx.step(lr, plateau_next if i == 0 else 0)
+            plateau = plateau_next if i == 0 else 0
+            rec = overlap.step(lr, plateau) if overlap is not None else ctx.step(lr, plateau)
             total += loss.detach().float()
             k += 1
         mean = total / a.steps_per_epoch
@@ -123,6 +124,10 @@ def main():
     ap.add_argument("--lr-warmup-epochs", type=int, default=1)
     ap.add_argument("--lr-factor", type=float, default=0.5)
     a = ap.parse_args()
+    if a.train_epochs and a.impl == "ddp":
+        raise SystemExit("--train-epochs drives the DASO schedule: use --impl daso or sync")
+    if a.overlap and a.mode != "faithful":
+        raise SystemExit("--overlap needs --mode faithful (bucketed node all-reduce)")
 
     import torch
     import torch.distributed as dist
@@ -204,7 +209,7 @@ def main():
         return loss
 
     if a.train_epochs and ctx is not None:
-        train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank)
+        train_loop(a, ctx, flat, net, images, labels, loss_fn, world, rank, overlap)
         ctx.finalize()
         if world > 1:
             dist.destroy_process_group()
