@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--S", type=int, default=1)
     ap.add_argument("--n", type=int, default=N_PARAMS)
     ap.add_argument("--topology", default="", help="PxG, default by --gpus")
-    ap.add_argument("--mode", choices=["faithful", "sharded", "fused", "nvls"], default="fused")
+    ap.add_argument("--mode", choices=["faithful", "sharded", "fused"], default="fused")
     ap.add_argument("--wire", choices=["bf16", "fp32"], default="bf16")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-e2e", action="store_true")
@@ -64,9 +64,11 @@ def parse():
     ap.add_argument("--compute-ms", type=float, default=0.0,
                     help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
                          "the global exchange the next batch's compute hides")
-    ap.add_argument("--overlap-compute-ms", type=float, default=20.0,
-                    help="fwd/bwd stand-in per batch inside the hidden-fraction cycles (P > 1)")
-    ap.add_argument("--cycles", type=int, default=8, help="B-cycles per leg of the hidden-fraction measurement")
+    ap.add_argument("--overlap-compute-ms", type=float, default=1.0,
+                    help="fwd/bwd stand-in per batch inside the hidden-fraction cycles (P > 1); config 3's "
+                         "real fwd/bwd (~55 ms at 256/GPU) hides the exchange trivially but drowns it in noise")
+    ap.add_argument("--cycles", type=int, default=30, help="B-cycles per leg of the hidden-fraction measurement")
+    ap.add_argument("--dump-steps", action="store_true", help="add every timed step's ms and kind to the line")
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline table (N=1)")
     ap.add_argument("--ref-div", type=int, default=4,
                     help="reference arm: oracle sample = n / ref-div parameters per step (scaled per parameter)")
@@ -308,58 +310,81 @@ def pct(xs, q):
     return xs[min(len(xs) - 1, int(q * len(xs)))] if xs else None
 
 
-def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle):
+def make_compute_small(ms: float, dev):
+    """Fine-grained fwd/bwd stand-in for the hidden-fraction cycles: bf16 4096^3 GEMMs (~0.1 ms
+    each) totalling ~ms, so legs with and without the exchange differ by little more than the
+    exchange itself."""
+    if ms <= 0:
+        return lambda: None
+    import torch
+    a = torch.randn(4096, 4096, device=dev, dtype=torch.bfloat16)
+    b = torch.randn_like(a)
+    c = torch.empty_like(a)
+    for _ in range(5):
+        torch.matmul(a, b, out=c)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        torch.matmul(a, b, out=c)
+    e1.record()
+    torch.cuda.synchronize()
+    reps = max(1, round(ms / (e0.elapsed_time(e1) / 20)))
+
+    def run():
+        for _ in range(reps):
+            torch.matmul(a, b, out=c)
+    return run
+
+
+def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t_ag):
     """SURVEY §8(d) hidden fraction: hidden = 1 - (T_with - T_without) / T_AG,alone, per B-cycle.
     One cycle = B batches of [fwd/bwd stand-in (bf16 GEMMs) ; gradient refresh ; daso_step], timed by
     CUDA events on the compute stream from the cycle's first batch to the end of its last.  In
     steady state every cycle contains exactly one merge, whose batch makes the compute stream wait
-    for its exchange (S <= B batches after the send), so each cycle's time includes exactly one
-    exchange's exposed part.  T_without: the same cycles with the group all-gather suppressed (daso_set_exchange(0)).
-    T_AG,alone: the all-gather alone (daso_exchange_alone)."""
+    for its exchange, so each cycle's time includes exactly one exchange's exposed part and any
+    slowdown the concurrent all-gather causes to the GEMMs and the fused kernels.  T_without: the
+    same cycles with the group all-gather suppressed (daso_set_exchange(0)).  The two legs
+    alternate block by block (a block is 1 cycle, or 2 when S = B so that the timed cycle's merge
+    waits for an exchange of its own leg) to cancel clock and power drift; T_AG,alone is measured
+    before the bench's first step (daso_exchange_alone)."""
     import torch
+    block = 1 if a.S < a.B else 2
 
-    def leg(enabled):
+    def batch():
+        compute()
+        g.copy_(g_src)
+        ctx.step(a.lr)
+
+    while ctx.query()["batch_in_cycle"] != a.B - 1:   # align: the next batch starts a cycle
+        batch()
+    legs = {True: [], False: []}
+    for c in range(2 * a.cycles):
+        enabled = c % 2 == 0
         ctx.set_exchange(enabled)
-        for _ in range(2 * a.B):                   # settle into the cycle with this setting
-            compute()
-            g.copy_(g_src)
-            ctx.step(a.lr)
-        while ctx.query()["batch_in_cycle"] != a.B - 1:
-            compute()
-            g.copy_(g_src)
-            ctx.step(a.lr)
-        torch.cuda.synchronize()
-        barrier(world)
-        ts = []
-        for _ in range(a.cycles):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+        for _ in range(block - 1):
             for _ in range(a.B):
-                compute()
-                g.copy_(g_src)
-                ctx.step(a.lr)
-            e1.record(stream)
-            ts.append((e0, e1))
-        torch.cuda.synchronize()
-        return [e0.elapsed_time(e1) for e0, e1 in ts]
-
-    t_with = leg(True)
-    t_without = leg(False)
+                batch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(a.B):
+            batch()
+        e1.record(stream)
+        legs[enabled].append((e0, e1))
     ctx.set_exchange(True)
     torch.cuda.synchronize()
-    barrier(world)
-    t_ag = ctx.exchange_alone(10)
+    t_with = [e0.elapsed_time(e1) for e0, e1 in legs[True]]
+    t_without = [e0.elapsed_time(e1) for e0, e1 in legs[False]]
     w_med = max_over_ranks(statistics.median(t_with), world)
     wo_med = max_over_ranks(statistics.median(t_without), world)
-    t_ag = max_over_ranks(t_ag, world)
-    exposed = max(0.0, w_med - wo_med)
-    hidden = 1.0 - exposed / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
-    return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); medians over cycles, "
-                   "max over ranks",
-            "cycles": a.cycles, "compute_ms_per_batch": a.overlap_compute_ms,
-            "T_cycle_with_ms": w_med, "T_cycle_without_ms": wo_med,
-            "T_cycle_with_p10_p90": [pct(t_with, 0.1), pct(t_with, 0.9)],
-            "T_cycle_without_p10_p90": [pct(t_without, 0.1), pct(t_without, 0.9)],
+    exposed = w_med - wo_med
+    hidden = 1.0 - max(0.0, exposed) / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
+    spread = max_over_ranks(pct(t_without, 0.9) - pct(t_without, 0.1), world)
+    return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); medians over "
+                   "alternating cycles, max over ranks; T_AG,alone before the first step",
+            "cycles_per_leg": a.cycles, "compute_ms_per_batch": a.overlap_compute_ms,
+            "T_cycle_with_ms": w_med, "T_cycle_without_ms": wo_med, "exposed_ms": exposed,
+            "T_cycle_without_p10_p90_spread_ms": spread,
             "T_AG_alone_ms": t_ag, "exchanges_per_cycle": n_exch_per_cycle, "hidden_fraction": hidden}
 
 
@@ -379,19 +404,16 @@ def run_ours(a):
                          steps_per_epoch=a.B * (1 << 20), momentum=0.9, weight_decay=1e-4, wire=a.wire,
                          mode=a.mode, nccl_max_ctas=a.nccl_max_ctas)
     n_pad = daso.daso_padded_numel(n, G)
-    if a.mode == "nvls":
-        x, g, v = ctx.alloc_bind(n)            # library-owned NCCL symmetric buckets
-    else:
-        x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
-        g = torch.zeros_like(x)
-        v = torch.zeros_like(x)
+    x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+    g = torch.zeros_like(x)
+    v = torch.zeros_like(x)
     x[:n] = torch.from_numpy(synthetic.microbench_x0(n)).to(dev)
     g_src = torch.zeros_like(x)
     l2_flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)   # 256 MB > 126 MB L2
     g_src[:n] = torch.from_numpy(synthetic.microbench_grad(n, rank, 0)).to(dev)
-    if a.mode != "nvls":
-        ctx.bind(x, g, v, n)
+    ctx.bind(x, g, v, n)
     stream = torch.cuda.current_stream()
+    t_ag = max_over_ranks(ctx.exchange_alone(10), world) if P > 1 else 0.0   # T_AG,alone: nothing in flight yet
 
     compute = make_compute(a.compute_ms, dev)
     for _ in range(a.warmup):
@@ -448,19 +470,15 @@ def run_ours(a):
         ms_launch = tr["kernel_ms"] / max(tr["kernel_launches"], 1)
         if ms_launch > 0:
             roofline["frac_in_kernel_dram"] = traffic / (ms_launch * 1e-3) / 1e9 / peak
-    if a.mode in ("fused", "nvls") and G > 1:
+    if a.mode == "fused" and G > 1:
         # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
         # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)
         nvl_bytes = 2.0 * (G - 1) * 4.0 * daso.daso_padded_numel(n, G) / G
-        if a.mode == "nvls":   # switch reads every element of this GPU's g + multicast store of the shard
-            nvl_bytes = 4.0 * daso.daso_padded_numel(n, G) * (1.0 + 1.0 / G)
         nvl_gbs = nvl_bytes / (tr["kernel_ms"] / max(tr["kernel_launches"], 1) * 1e-3) / 1e9
         nvl_gbs = -max_over_ranks(-nvl_gbs, world)
         roofline = {"bound": "nvlink", "achieved": nvl_gbs, "peak": 770.0, "unit": "GB/s",
                     "frac": nvl_gbs / 770.0, "traffic": None,
-                    "kernel": ("nvls_kernel (node gradient reduce in the NVSwitch by multimem.ld_reduce + update "
-                               "[+merge] [+pack] + parameter broadcast by multimem.st)") if a.mode == "nvls" else
-                              ("peer_kernel (node gradient reduce over NVLink + update [+merge] [+pack] + "
+                    "kernel": ("peer_tma_kernel (node gradient reduce over NVLink + update [+merge] [+pack] + "
                                "parameter all-gather by NVLink stores)"),
                     "bytes_per_launch": nvl_bytes, "bytes_def": "NVLink bytes per direction per GPU",
                     "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1),
@@ -485,7 +503,8 @@ def run_ours(a):
     overlap = None
     if P > 1:
         nx = 1 if a.S > 0 else a.B          # exchanges issued per B-cycle
-        overlap = overlap_cycles(ctx, a, g, g_src, stream, world, make_compute(a.overlap_compute_ms, dev), nx)
+        overlap = overlap_cycles(ctx, a, g, g_src, stream, world, make_compute_small(a.overlap_compute_ms, dev), nx,
+                                 t_ag)
 
     # ---- e2e through the C ABI with host buffers (daso_step_host) -------------------------------
     e2e = None
@@ -538,6 +557,7 @@ def run_ours(a):
                                        "timing with the exchange inside the window is `overlap`",
                        "compute_ms_between_steps": a.compute_ms},
             "step_kinds": kinds_max, "overlap": overlap, "kernels": kernels,
+            "steps_dump": ({"ms": step_ms, "kind": kind_of} if a.dump_steps else None),
             "roofline": roofline, "phases": phases, "gpu_launches": launches_total,
             "gpu_launches_per_rank": tr["kernel_launches"],
             "clocks": clk.summary(), "e2e": e2e, "finite": finite}

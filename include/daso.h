@@ -51,10 +51,9 @@ enum { DASO_MODE_FAITHFUL = 0,  /* v1: rotating group exchange + node broadcast 
        DASO_MODE_FUSED = 2,     /* v3: the sharded batch with the node tier (gradient reduce over
                                    peers + update/merge/pack + parameter all-gather) in ONE kernel
                                    over NVLink peer memory (CUDA IPC); G <= 8; caller buffers must
-                                   be cudaMalloc-backed (torch's default allocator is) */
-       DASO_MODE_NVLS = 3 };    /* v4: as FUSED, but the gradient reduce runs inside the NVSwitch
-                                   (multimem.ld_reduce) and the parameter shard is broadcast by one
-                                   multimem.st; buckets must come from daso_alloc_bind */
+                                   be cudaMalloc-backed (torch's default allocator is) or come from
+                                   daso_alloc_bind.  (Value 3, an NVSwitch-multicast variant of
+                                   round 1, was measured slower and removed: DESIGN.md §7.) */ };
 
 const char* daso_status_string(daso_status s);
 const char* daso_version(void);
@@ -133,7 +132,7 @@ typedef struct {
     float   momentum;         /* mu, P:172 uses 0.9 */
     float   weight_decay;     /* wd, P:172 uses 1e-4 */
     int32_t wire;             /* DASO_WIRE_BF16 (default) or DASO_WIRE_FP32 (R3) */
-    int32_t mode;             /* DASO_MODE_FAITHFUL / _SHARDED / _FUSED / _NVLS (see the enum above) */
+    int32_t mode;             /* DASO_MODE_FAITHFUL / _SHARDED / _FUSED (see the enum above) */
     int32_t check_finite;     /* 1 = fused non-finite flag in every update kernel */
     int32_t nccl_max_ctas;    /* >0: cap NCCL CTAs on the group (side-stream) comm to leave SMs to compute; 0 = NCCL default */
 } daso_config;
@@ -154,7 +153,7 @@ daso_status daso_init(daso_ctx** out, int world, int gpus_per_node, int B, int S
                       const daso_config* cfg, const void* nccl_uid128);
 
 /* n rounded up to a multiple of 64 * gpus_per_node: the bucket capacity the sharded,
- * fused and nvls modes require (shards of n_pad / G elements, 256-byte aligned). */
+ * and fused modes require (shards of n_pad / G elements, 256-byte aligned). */
 size_t daso_padded_numel(size_t n, int gpus_per_node);
 
 /* Attach the caller's flat fp32 buckets ("buffer packaging"): params x[n],
@@ -167,19 +166,17 @@ size_t daso_padded_numel(size_t n, int gpus_per_node);
  * identical on every rank (R17) and v zero-initialised by the caller.  The library
  * allocates its exchange slot here: [P][seg] wire elements (seg = n_pad in the faithful
  * mode, n_pad / G otherwise; n_pad = n rounded up to 64 * G).  Errors:
- * DASO_ERR_PROTOCOL (bound twice; DASO_MODE_NVLS with G > 1, which needs
- * daso_alloc_bind), DASO_ERR_ARGUMENT (null, n = 0, misaligned, not a device allocation
- * in the fused mode), DASO_ERR_CUDA / DASO_ERR_NCCL. */
+ * DASO_ERR_PROTOCOL (bound twice), DASO_ERR_ARGUMENT (null, n = 0, misaligned; in the
+ * fused mode: not a device allocation, or memory CUDA IPC cannot export — cuMem /
+ * expandable_segments — use daso_alloc_bind), DASO_ERR_CUDA / DASO_ERR_NCCL. */
 daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n);
 
-/* Allocate the flat buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed) in
- * library-owned memory and bind them; returns the device pointers (owned by the library,
- * valid until daso_finalize).  DASO_MODE_NVLS (G > 1): x and g are NCCL symmetric memory
- * (ncclMemAlloc) registered as windows on the node communicator, which NVLS requires for
- * its multicast addresses; every other mode: cudaMalloc (what the fused mode's CUDA IPC
- * export needs — use this when the caller's allocator hands out cuMem memory, e.g.
- * PYTORCH_CUDA_ALLOC_CONF=expandable_segments:True).  Collective over the node.  Errors: as daso_bind; DASO_ERR_CONFIG if the node
- * has no NVLS multicast support (NVLS mode). */
+/* Allocate the flat buckets x, g, v (daso_padded_numel(n, G) fp32 each, zeroed) with
+ * cudaMalloc and bind them; returns the device pointers (owned by the library, valid until
+ * daso_finalize).  The fused mode's CUDA IPC export needs cudaMalloc memory: use this when
+ * the caller's allocator hands out cuMem memory (e.g. PYTORCH_CUDA_ALLOC_CONF=
+ * expandable_segments:True).  Collective over the node in the fused mode.  Errors: as
+ * daso_bind. */
 daso_status daso_alloc_bind(daso_ctx* c, size_t n, float** x, float** g, float** v);
 
 /* ----- split API (each a collective over the world; what daso_step composes) -----
@@ -204,8 +201,8 @@ daso_status daso_global_merge(daso_ctx* c, void* stream);
  * advance the schedule (record in *out if non-null), node all-reduce of g, the fused
  * update (+ Eq. (1) merge if due) (+ wire pack if this rank sends) kernel, node
  * broadcast after a merge, side-stream group all-gather for a send, and — blocking
- * — the average kernel and broadcast.  Sharded / fused / nvls modes run the same batch
- * element-sharded over the node; fused and nvls put the whole node tier
+ * — the average kernel and broadcast.  Sharded / fused modes run the same batch
+ * element-sharded over the node; fused puts the whole node tier
  * in one kernel.  `lr` is this batch's learning rate; `plateau` as in daso_sched_next.
  * Errors: DASO_ERR_PROTOCOL (not bound; schedule/flight-state mismatch), asynchronous
  * DASO_ERR_CUDA / DASO_ERR_NCCL from earlier work. */

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libdaso.so")
 OK, ERR_CONFIG, ERR_RANGE, ERR_PROTOCOL, ERR_ARGUMENT, ERR_CUDA, ERR_NCCL, ERR_NONFINITE = range(8)
 WARMUP, CYCLING, COOLDOWN = 0, 1, 2
 WIRE_BF16, WIRE_FP32 = 0, 1
-MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED, MODE_NVLS = 0, 1, 2, 3
+MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED = 0, 1, 2
 STEP_GRADS_REDUCED = 1
 
 

@@ -59,12 +59,8 @@ struct daso_ctx {
     unsigned long long epoch = 0;
     std::vector<void*> ipc_opened;
 
-    // library-owned buckets (daso_alloc_bind): NCCL symmetric memory for NVLS, cudaMalloc otherwise
-    void* own_nccl[3] = {};
+    // library-owned buckets (daso_alloc_bind, cudaMalloc)
     void* own_cuda[3] = {};
-    daso::NvlsBuckets nvls{};
-    float* x_mc = nullptr;   // multicast (NVLS) address of x
-    float* g_mc = nullptr;   // multicast (NVLS) address of g
 
     // virtual cluster (daso_vcluster_*): this ctx is one of W virtual ranks on ONE GPU; the
     // group all-gather and the blocking tail are run by the cluster driver after every rank's
@@ -445,18 +441,8 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
         const double wb = double(c->wire_bytes);
         double per = 20.0 + 8.0 * (c->G - 1) + ((ops & daso::OP_MERGE) ? c->P * wb : 0) +
                      ((ops & daso::OP_PACK) ? wb : 0);
-        if (c->cfg.mode == DASO_MODE_NVLS) {
-            // HBM on this GPU: own x r + v rw (12) + the switch reading this GPU's g for every
-            // shard (4 G) + the multicast stores of all G shards into this GPU's x (4 G)
-            per = 12.0 + 8.0 * c->G + ((ops & daso::OP_MERGE) ? c->P * wb : 0) + ((ops & daso::OP_PACK) ? wb : 0);
-            pa.x_mc = c->x_mc + off;
-            pa.g_mc = c->g_mc + off;
-        }
         Span sp(c, s, PH_KERNEL, per * double(sh));
-        if (c->cfg.mode == DASO_MODE_NVLS)
-            KERN_TRY(c, daso::launch_nvls(ops, c->cfg.wire, pa, s));
-        else
-            KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
+        KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
     }
     if (send) {
         STATUS_TRY(start_exchange(c, s));
@@ -497,7 +483,7 @@ struct IpcExport {
     uint64_t off[3];
 };
 
-daso_status setup_peers(daso_ctx* c, bool sig_only) {
+daso_status setup_peers(daso_ctx* c) {
     PfnAddressRange range = address_range_fn();
     if (!range) return c->fail(DASO_ERR_CUDA, "cuMemGetAddressRange unavailable");
     const size_t sig_bytes = (2 * size_t(c->G) + 2) * sizeof(unsigned long long);
@@ -505,7 +491,7 @@ daso_status setup_peers(daso_ctx* c, bool sig_only) {
     CUDA_TRY(c, cudaMemset(c->sig, 0, sig_bytes));
     void* bufs[3] = {c->x, c->g, c->sig};
     IpcExport mine{};
-    for (int b = sig_only ? 2 : 0; b < 3; ++b) {
+    for (int b = 0; b < 3; ++b) {
         CUdeviceptr base = 0;
         size_t size = 0;
         if (range(&base, &size, CUdeviceptr(bufs[b])) != CUDA_SUCCESS)
@@ -534,8 +520,8 @@ daso_status setup_peers(daso_ctx* c, bool sig_only) {
         if (q == c->local) {
             for (int b = 0; b < 3; ++b) mapped[b] = reinterpret_cast<char*>(bufs[b]) - all[q].off[b];
         } else {
-            for (int b = sig_only ? 2 : 0; b < 3; ++b) {
-                for (int e = sig_only ? 2 : 0; e < b; ++e)   // one mapping per distinct allocation of the peer
+            for (int b = 0; b < 3; ++b) {
+                for (int e = 0; e < b; ++e)   // one mapping per distinct allocation of the peer
                     if (all[q].base[e] == all[q].base[b]) mapped[b] = mapped[e];
                 if (!mapped[b]) {
                     CUDA_TRY(c, cudaIpcOpenMemHandle(&mapped[b], all[q].h[b], cudaIpcMemLazyEnablePeerAccess));
@@ -543,10 +529,8 @@ daso_status setup_peers(daso_ctx* c, bool sig_only) {
                 }
             }
         }
-        if (!sig_only) {
-            c->peer_x[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[0]) + all[q].off[0]);
-            c->peer_g[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[1]) + all[q].off[1]);
-        }
+        c->peer_x[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[0]) + all[q].off[0]);
+        c->peer_g[q] = reinterpret_cast<float*>(static_cast<char*>(mapped[1]) + all[q].off[1]);
         c->peer_sig[q] = reinterpret_cast<unsigned long long*>(static_cast<char*>(mapped[2]) + all[q].off[2]);
     }
     return DASO_OK;
@@ -597,10 +581,9 @@ daso_status make_ctx(daso_ctx** out, int world, int gpus_per_node, int B, int S,
     if (world < 1 || gpus_per_node < 1 || world % gpus_per_node != 0 || B < 1) return DASO_ERR_CONFIG;
     if (cfg->rank < 0 || cfg->rank >= world) return DASO_ERR_RANGE;
     if (cfg->wire != DASO_WIRE_BF16 && cfg->wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
-    if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED && cfg->mode != DASO_MODE_FUSED &&
-        cfg->mode != DASO_MODE_NVLS)
+    if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED && cfg->mode != DASO_MODE_FUSED)
         return DASO_ERR_ARGUMENT;
-    if ((cfg->mode == DASO_MODE_FUSED || cfg->mode == DASO_MODE_NVLS) && gpus_per_node > daso::kMaxPeers)
+    if (cfg->mode == DASO_MODE_FUSED && gpus_per_node > daso::kMaxPeers)
         return DASO_ERR_CONFIG;
     daso_sched_config sc{};
     sc.B_init = B;
@@ -671,8 +654,6 @@ daso_status bind_impl(daso_ctx* c, float* x, float* g, float* v, size_t n);
 
 daso_status daso_bind(daso_ctx* c, float* x, float* g, float* v, size_t n) {
     if (!c) return DASO_ERR_ARGUMENT;
-    if (c->cfg.mode == DASO_MODE_NVLS && c->G > 1)
-        return c->fail(DASO_ERR_PROTOCOL, "DASO_MODE_NVLS needs library-owned buckets: use daso_alloc_bind");
     return bind_impl(c, x, g, v, n);
 }
 
@@ -681,36 +662,15 @@ daso_status daso_alloc_bind(daso_ctx* c, size_t n, float** x, float** g, float**
     if (c->bound) return c->fail(DASO_ERR_PROTOCOL, "daso_bind called twice");
     const size_t n_pad = daso_padded_numel(n, c->G);
     const size_t bytes = (n_pad * sizeof(float) + (size_t(2) << 20) - 1) / (size_t(2) << 20) * (size_t(2) << 20);
-    // NVLS needs NCCL symmetric memory (ncclMemAlloc: cuMem-backed, multicast-capable); every
-    // other mode gets plain cudaMalloc, which the fused mode's CUDA IPC export requires.
-    const bool sym = c->cfg.mode == DASO_MODE_NVLS && c->G > 1;
     void* p[3] = {nullptr, nullptr, nullptr};
-    for (int b = 0; b < 3; ++b) {
-        if (sym && b < 2) {
-            NCCL_TRY(c, ncclMemAlloc(&p[b], bytes));
-            c->own_nccl[b] = p[b];
-        } else {
-            CUDA_TRY(c, cudaMalloc(&p[b], bytes));
-            c->own_cuda[b] = p[b];
-        }
+    for (int b = 0; b < 3; ++b) {   // cudaMalloc: what the fused mode's CUDA IPC export needs
+        CUDA_TRY(c, cudaMalloc(&p[b], bytes));
+        c->own_cuda[b] = p[b];
         CUDA_TRY(c, cudaMemset(p[b], 0, bytes));
     }
     c->x = static_cast<float*>(p[0]);
     c->g = static_cast<float*>(p[1]);
     c->v = static_cast<float*>(p[2]);
-    if (sym) {
-        const char* why = nullptr;
-        const int r = daso::nvls_setup(c->node_comm, p[0], p[1], bytes, c->G, &c->nvls, &why);
-        if (r == 1) return c->fail(DASO_ERR_NCCL, "NVLS setup: %s", why);
-        if (r == 2) return c->fail(DASO_ERR_CONFIG, "NVLS setup: %s", why);
-        if (r == 3) return c->fail(DASO_ERR_CUDA, "NVLS setup: %s", why);
-        c->x_mc = c->nvls.x_mc;
-        c->g_mc = c->nvls.g_mc;
-        for (int q = 0; q < c->G; ++q) {   // load-store-accessible peer addresses (blocking path)
-            c->peer_x[q] = c->nvls.peer_x[q];
-            c->peer_g[q] = c->nvls.peer_g[q];
-        }
-    }
     STATUS_TRY(bind_impl(c, c->x, c->g, c->v, n));
     *x = c->x;
     *g = c->g;
@@ -735,8 +695,7 @@ daso_status bind_impl(daso_ctx* c, float* x, float* g, float* v, size_t n) {
         CUDA_TRY(c, cudaMalloc(&c->slot, bytes));
         CUDA_TRY(c, cudaMemset(c->slot, 0, bytes));
     }
-    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1 && !c->vc) STATUS_TRY(setup_peers(c, false));
-    if (c->cfg.mode == DASO_MODE_NVLS && c->G > 1) STATUS_TRY(setup_peers(c, true));
+    if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1 && !c->vc) STATUS_TRY(setup_peers(c));
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->bound = true;
     return DASO_OK;
@@ -840,7 +799,7 @@ daso_status daso_step_ex(daso_ctx* c, float lr, int plateau, int flags, void* st
     if (r.merge && c->P > 1 && !c->inflight)
         return c->fail(DASO_ERR_PROTOCOL, "schedule merge at step %lld but nothing in flight", (long long)r.step);
     if (c->cfg.mode == DASO_MODE_SHARDED) return step_sharded(c, r, lr, s);
-    if (c->cfg.mode == DASO_MODE_FUSED || c->cfg.mode == DASO_MODE_NVLS) return step_fused(c, r, lr, s);
+    if (c->cfg.mode == DASO_MODE_FUSED) return step_fused(c, r, lr, s);
     return step_faithful(c, r, lr, s, reduced);
 }
 
@@ -968,12 +927,9 @@ daso_status daso_finalize(daso_ctx* c) {
         for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
         if (c->sig) cudaFree(c->sig);
     }
-    daso::nvls_teardown(c->node_comm, &c->nvls);
     cudaDeviceSynchronize();
-    for (int b = 0; b < 3; ++b) {
-        if (c->own_nccl[b]) ncclMemFree(c->own_nccl[b]);
+    for (int b = 0; b < 3; ++b)
         if (c->own_cuda[b]) cudaFree(c->own_cuda[b]);
-    }
     ncclComm_t comms[4] = {c->bucket_comm, c->group_comm, c->node_comm, c->world_comm};
     for (ncclComm_t m : comms) {
         if (!m) continue;
@@ -1018,7 +974,6 @@ daso_status daso_vcluster_create(daso_vcluster** out, int world, int gpus_per_no
     *out = nullptr;
     const bool fused = cfg->mode == DASO_MODE_FUSED;
     if (!fused && gpus_per_node != 1) return DASO_ERR_CONFIG;   // NCCL node collectives cannot loop back
-    if (cfg->mode == DASO_MODE_NVLS) return DASO_ERR_CONFIG;
     daso_vcluster* v = new (std::nothrow) daso_vcluster;
     if (!v) return DASO_ERR_ARGUMENT;
     *out = v;

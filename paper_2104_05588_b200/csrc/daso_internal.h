@@ -62,28 +62,12 @@ struct PeerArgs {
     unsigned long long* sig_me = nullptr;      // this rank's signal array
     unsigned* done = nullptr;                  // this rank's CTA completion counter
     uint32_t* err = nullptr;                   // bit 1 set on a barrier timeout
-    float* x_mc = nullptr;                     // NVLS: multicast address of x at this shard
-    const float* g_mc = nullptr;               // NVLS: multicast address of g at this shard
     unsigned long long epoch = 0;              // monotonically increasing barrier value
     unsigned long long timeout_ns = 20ull * 1000 * 1000 * 1000;   // barrier wait limit (then bit 1 of err)
     int G = 1, me = 0;
 };
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream);
 
-// NVLS buckets (nvls_host.cpp, host-only C++ against NCCL's symmetric-memory / device-comm API)
-struct NvlsBuckets {
-    void* win_x = nullptr;       // ncclWindow_t
-    void* win_g = nullptr;
-    void* devcomm = nullptr;     // heap copy of ncclDevComm
-    float* x_mc = nullptr;
-    float* g_mc = nullptr;
-    float* peer_x[kMaxPeers] = {};
-    float* peer_g[kMaxPeers] = {};
-};
-// returns 0 ok, 1 NCCL error, 2 no multicast support, 3 CUDA error; *why = message
-int nvls_setup(void* node_comm, void* x, void* g, size_t bytes, int G, NvlsBuckets* out, const char** why);
-void nvls_teardown(void* node_comm, NvlsBuckets* b);
-int launch_nvls(int ops, int wire, const PeerArgs& pa, void* stream);
 int set_kernel_impl(int impl);   // returns the previous selection
 int current_kernel_impl();       // 0 register path, 1 TMA-staged path
 int launch_gather(const float* const* src, const size_t* numel, const size_t* offsets, int count,

@@ -80,7 +80,9 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
 }
 
 // Eight parameters per thread for every op set.  Measured alternatives (profiles/r01): 32 per
-// thread for the light kernels (average, pack) was slower (K4 41 -> 57 us, pack 23 -> 37 us), and
+// thread for the light kernels (average, pack) was slower (K4 41 -> 57 us, pack 23 -> 37 us); a
+// K4 with P templated and two chunks per thread, all 2P row loads in flight before the sums, ran
+// 42.0 vs 42.4 us at P = 2 and 57.6 vs 53.2 us at P = 4 (profiles/r02/k4_variants.txt), and
 // issuing the two 128-bit loads of a stream from an array loop instead of two named loads cost K1
 // 9 % (75 -> 82 us, same box, A/B in one run): ptxas schedules the explicit form better.
 template <int OPS, int WIRE>

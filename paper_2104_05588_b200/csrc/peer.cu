@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "daso_internal.h"
 #include "device_common.cuh"
@@ -323,6 +324,15 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
     end_barrier(pa, G);
 }
 
+int peer_tma_ctas() {   // DASO_PEER_TMA_CTAS, 0 = default (SMs - 16)
+    static int ctas = -1;
+    if (ctas < 0) {
+        const char* e = getenv("DASO_PEER_TMA_CTAS");
+        ctas = e ? std::max(1, atoi(e)) : 0;
+    }
+    return ctas;
+}
+
 template <int OPS, int WIRE, int G>
 int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
@@ -341,14 +351,181 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     // DASO_PEER_TMA_CTAS: persistent CTAs.  Default: one per SM minus 16, so the side-stream
     // exchange's NCCL kernels always find free SMs (2x2: exchange hidden 0.98 vs 0.73 with every
     // SM taken, same kernel time; profiles/r01/b20_*).
-    static int ctas = -1;
-    if (ctas < 0) {
-        const char* e = getenv("DASO_PEER_TMA_CTAS");
-        ctas = e ? std::max(1, atoi(e)) : 0;
-    }
-    const int grid = ctas > 0 ? std::min(ctas, sms) : std::max(1, sms - 16);
+    const int grid = peer_tma_ctas() > 0 ? std::min(peer_tma_ctas(), sms) : std::max(1, sms - 16);
     peer_tma_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
+}
+
+// ---- warp-specialised TMA variant (DASO_PEER=ws): the same batch and arithmetic as
+// peer_tma_kernel, with the data movement decoupled from the compute by mbarriers instead of
+// CTA-wide barriers.  9 warps: warps 0-7 compute (8 parameters per thread of a 2048-parameter
+// tile), warp 8 lane 0 is the TMA engine driver:
+//   full[s]   (tx bytes)  stage s holds tile k's own x, v, the G gradient tiles (+ slot rows);
+//   ofull[o]  (8 arrivals) the compute warps have consumed stage k % NS and written tile k's
+//                          new x, v (+ packed row) into output buffer o = k % NO;
+//   oempty[o] (1 arrival)  the bulk stores issued from output buffer o have read it.
+// The driver refills a stage as soon as its tile is computed and issues the stores of every
+// output buffer as soon as it is written, so NVLink reads, NVLink stores and compute of
+// different tiles overlap continuously; no thread ever waits for the whole CTA.
+constexpr int kWsCompute = 256, kWsThreads = kWsCompute + 32, kWsOut = 2;
+
+template <int OPS, int WIRE, int G>
+__global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs pa, int NS) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const KernelArgs& a = pa.a;
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, a.P, wb);
+    unsigned char* outs = smem + size_t(NS) * L.in_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(kWsOut) * L.out_bytes);
+    uint64_t* ofull = full + NS;
+    uint64_t* oempty = ofull + kWsOut;
+    const int tid = threadIdx.x;
+    if (!start_barrier(pa, G)) return;   // 1. start barrier (timed out: error bit raised, do nothing)
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        for (int o = 0; o < kWsOut; ++o) {
+            mbar_init(&ofull[o], kWsCompute / 32);
+            mbar_init(&oempty[o], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_global();
+    }
+    __syncthreads();
+    const int64_t ntiles = a.n / kPT;
+    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto tile0 = [&](int64_t k) { return (int64_t(blockIdx.x) + k * gridDim.x) * kPT; };
+    bool bad = false;
+    if (tid == kWsCompute) {   // ---- the TMA driver
+        auto issue_load = [&](int64_t k) {
+            const int s = int(k % NS);
+            unsigned char* st = smem + size_t(s) * L.in_bytes;
+            const int64_t e0 = tile0(k);
+            uint32_t tx = (2u + G) * kPT * 4u;
+            if constexpr ((OPS & OP_MERGE) != 0) tx += uint32_t(a.P) * kPT * wb;
+            mbar_expect_tx(&full[s], tx);
+#pragma unroll
+            for (int q = 0; q < G; ++q) {                       // start with the next peer: spread links
+                const int qq = (pa.me + 1 + q) % G;
+                bulk_g2s(st + L.g + uint32_t(qq) * kPT * 4, pa.gp[qq] + e0, kPT * 4, &full[s]);
+            }
+            bulk_g2s(st + L.x, a.x + e0, kPT * 4, &full[s]);
+            bulk_g2s(st + L.v, a.v + e0, kPT * 4, &full[s]);
+            if constexpr ((OPS & OP_MERGE) != 0) {
+                for (int p = 0; p < a.P; ++p)
+                    bulk_g2s(st + L.slot + uint32_t(p) * kPT * wb,
+                             static_cast<const unsigned char*>(a.slot) + (p * a.slot_stride + e0) * wb, kPT * wb,
+                             &full[s]);
+            }
+        };
+        for (int64_t k = 0; k < my && k < NS; ++k) issue_load(k);
+        for (int64_t k = 0; k < my; ++k) {
+            const int o = int(k % kWsOut);
+            if (!mbar_wait(&ofull[o], uint32_t((k / kWsOut) & 1), pa.err)) break;
+            if (k + NS < my) issue_load(k + NS);                // stage k % NS consumed: refill it
+            unsigned char* ob = outs + size_t(o) * L.out_bytes;
+            const int64_t e0 = tile0(k);
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const int qq = (pa.me + 1 + q) % G;
+                bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
+            }
+            bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
+            if constexpr ((OPS & OP_PACK) != 0)
+                bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, ob + L.opack, kPT * wb);
+            bulk_commit();
+            if (k >= 1) {                                       // the previous tile's buffer has been read
+                bulk_wait_read<1>();
+                mbar_arrive(&oempty[(k - 1) % kWsOut]);
+            }
+        }
+        bulk_wait_all();
+    } else if (tid < kWsCompute) {   // ---- compute warps
+        for (int64_t k = 0; k < my; ++k) {
+            const int s = int(k % NS), o = int(k % kWsOut);
+            unsigned char* st = smem + size_t(s) * L.in_bytes;
+            unsigned char* ob = outs + size_t(o) * L.out_bytes;
+            if (!mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err)) break;
+            const int i = tid * 8;
+            float x[8], v[8], g[8];
+            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.x, i, x);
+            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.v, i, v);
+            Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g, i, g);
+#pragma unroll
+            for (int q = 1; q < G; ++q) {
+                float t[8];
+                Wire<DASO_WIRE_FP32>::template load_smem<8>(st + L.g + uint32_t(q) * kPT * 4, i, t);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] += t[j];                        // ascending local id (R18)
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
+                v[j] = fmaf(a.mu, v[j], d);
+                x[j] = fmaf(-a.lr, v[j], x[j]);
+            }
+            if constexpr ((OPS & OP_MERGE) != 0) {
+                float acc[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+                for (int p = 0; p < a.P; ++p) {
+                    float sv[8];
+                    Wire<WIRE>::template load_smem<8>(st + L.slot + uint32_t(p) * kPT * wb, i, sv);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j] += sv[j] - x[j];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
+            }
+            if (k >= kWsOut && !mbar_wait(&oempty[o], uint32_t(((k / kWsOut) - 1) & 1), pa.err)) break;
+            Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
+            Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
+            if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
+            fence_async_smem();                                  // generic-proxy writes -> bulk stores
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&ofull[o]);
+        }
+        if (blockIdx.x == gridDim.x - 1)                         // ragged tail through the register path
+            for (int64_t e = ntiles * kPT + tid; e < a.n; e += kWsCompute) peer_body<OPS, WIRE, G, 1>(pa, e, bad);
+        if (a.flag != nullptr) {
+            const unsigned any = __ballot_sync(0xffffffffu, bad);
+            if (any != 0u && (tid & 31) == 0) atomicOr(a.flag, 1u);
+        }
+    }
+    // 3. end barrier (the driver has waited for all its bulk stores: wait_group 0)
+    if (tid == kWsCompute) fence_proxy_async_global();
+    end_barrier(pa, G);
+}
+
+template <int OPS, int WIRE, int G>
+int launch_peer_ws_t(const PeerArgs& pa, cudaStream_t s, int sms) {
+    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
+    const PeerTmaLayout L = peer_tma_layout(OPS, G, pa.a.P, wb);
+    const int budget = 210 * 1024 - kWsOut * int(L.out_bytes);
+    const int NS = int(std::min<int64_t>(8, (budget - 128) / L.in_bytes));
+    if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
+    const size_t smem = size_t(NS) * L.in_bytes + size_t(kWsOut) * L.out_bytes + 8 * size_t(NS + 2 * kWsOut);
+    static size_t attr = 0;
+    if (smem > attr) {
+        const cudaError_t e = cudaFuncSetAttribute(peer_ws_kernel<OPS, WIRE, G>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return int(e);
+        attr = smem;
+    }
+    const int grid = peer_tma_ctas() > 0 ? std::min(peer_tma_ctas(), sms) : std::max(1, sms - 16);
+    peer_ws_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kWsThreads), smem, s>>>(pa, NS);
+    return int(cudaGetLastError());
+}
+
+// Peer data path under daso_kernel_impl(2) "auto" (DASO_PEER=ws|tma|ldg).
+int peer_path() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("DASO_PEER");
+        v = (e && strcmp(e, "ldg") == 0) ? 0 : (e && strcmp(e, "tma") == 0) ? 1 : 2;
+    }
+    return v;
 }
 
 template <int OPS, int WIRE, int G>
@@ -356,7 +533,10 @@ int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
     const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
                       reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
     // TMA unless the register path is forced (daso_kernel_impl(0))
-    if (current_kernel_impl() != 0 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
+    const int impl = current_kernel_impl();   // 0 register, 1 TMA, 2 auto (DASO_PEER, default ws)
+    const int path = impl == 2 ? peer_path() : impl == 1 ? 1 : 0;
+    if (path == 2 && al && pa.a.n >= kPT) return launch_peer_ws_t<OPS, WIRE, G>(pa, s, sms);
+    if (path == 1 && al && pa.a.n >= kPT) return launch_peer_tma_t<OPS, WIRE, G>(pa, s, sms);
     return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
 }
 
@@ -387,187 +567,7 @@ int dispatch_peer(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
 }
 
 
-// ---- NVLS variant (DASO_MODE_NVLS; SURVEY §8(f) N1 as specified): the node gradient
-// reduce is done inside the NVSwitch — multimem.ld_reduce on the multicast address of g
-// returns the sum over the node's G GPUs of this shard — and the new parameter shard is
-// written to every GPU of the node by ONE multimem.st through the switch.  Per GPU and
-// direction 4n(1 + 1/G) bytes cross NVLink instead of 8n(G-1)/G (fewer for G >= 4).
-// The switch's summation order is fixed by the hardware, not ascending local id (R18);
-// each element's sum is formed once, so node replicas stay bitwise identical.
-__device__ __forceinline__ float4 mm_ld_reduce_add(const float* p) {
-    float4 r;
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                 : "l"(p)
-                 : "memory");
-    return r;
-}
-__device__ __forceinline__ float mm_ld_reduce_add1(const float* p) {
-    float r;
-    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
-    return r;
-}
-__device__ __forceinline__ void mm_st(float* p, float4 v) {
-    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
-                 "f"(v.z), "f"(v.w)
-                 : "memory");
-}
-__device__ __forceinline__ void mm_st1(float* p, float v) {
-    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
-}
-
-template <int OPS, int WIRE, int N>
-__device__ __forceinline__ void nvls_body(const PeerArgs& pa, int64_t i, bool& bad) {
-    const KernelArgs& a = pa.a;
-    float x[N], v[N], g[N];
-    if constexpr (N % 4 == 0) {
-        float4 gv[N / 4];
-#pragma unroll
-        for (int q = 0; q < N / 4; ++q) gv[q] = mm_ld_reduce_add(pa.g_mc + i + 4 * q);   // all in flight
-#pragma unroll
-        for (int q = 0; q < N / 4; ++q) {
-            g[4 * q] = gv[q].x; g[4 * q + 1] = gv[q].y; g[4 * q + 2] = gv[q].z; g[4 * q + 3] = gv[q].w;
-        }
-#pragma unroll
-        for (int q = 0; q < N / 8; ++q) {
-            float xt[8], vt[8];
-            ld_f32<8>(a.x + i + 8 * q, xt);
-            ld_f32<8>(a.v + i + 8 * q, vt);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { x[8 * q + j] = xt[j]; v[8 * q + j] = vt[j]; }
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < N; ++j) g[j] = mm_ld_reduce_add1(pa.g_mc + i + j);
-        ld_f32<N>(a.x + i, x);
-        ld_f32<N>(a.v + i, v);
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const float d = fmaf(a.wd, x[j], g[j] * a.gscale);
-        v[j] = fmaf(a.mu, v[j], d);
-        x[j] = fmaf(-a.lr, v[j], x[j]);
-    }
-    if constexpr (N % 8 == 0) {
-#pragma unroll
-        for (int q = 0; q < N / 8; ++q) {
-            float vt[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) vt[j] = v[8 * q + j];
-            st_f32<8>(a.v + i + 8 * q, vt);
-        }
-    } else {
-        st_f32<N>(a.v + i, v);
-    }
-    if constexpr ((OPS & OP_MERGE) != 0) {
-        float acc[N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) acc[j] = 0.f;
-#pragma unroll 2
-        for (int p = 0; p < a.P; ++p) {
-#pragma unroll
-            for (int q = 0; q < (N + 7) / 8; ++q) {
-                constexpr int M = N < 8 ? N : 8;
-                float s[M];
-                Wire<WIRE>::template load<M>(a.slot, p * a.slot_stride + i + 8 * q, s);
-#pragma unroll
-                for (int j = 0; j < M; ++j) acc[8 * q + j] += s[j] - x[8 * q + j];
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;
-    }
-    if constexpr (N % 4 == 0) {
-#pragma unroll
-        for (int q = 0; q < N / 4; ++q)
-            mm_st(pa.x_mc + i + 4 * q, make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
-    } else {
-#pragma unroll
-        for (int j = 0; j < N; ++j) mm_st1(pa.x_mc + i + j, x[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
-    if constexpr ((OPS & OP_PACK) != 0) {
-#pragma unroll
-        for (int q = 0; q < (N + 7) / 8; ++q) {
-            constexpr int M = N < 8 ? N : 8;
-            float t[M];
-#pragma unroll
-            for (int j = 0; j < M; ++j) t[j] = x[8 * q + j];
-            Wire<WIRE>::template store<M>(a.pack_out, i + 8 * q, t);
-        }
-    }
-}
-
-constexpr int kNV = 8;   // parameters per thread per iteration: 2 multimem.ld_reduce.v4 in flight
-
-// Total CTAs of the NVLS kernel (DASO_NVLS_CTAS, default 296 = 2 per SM).  Measured at 1x4
-// (profiles/r01/b17_*, b18_*): 32..296 CTAs x 2 reduces in flight all run at ~0.43 of the link,
-// 16 CTAs at 0.29, 1184 CTAs x 4 reduces at 0.19-0.23 — the multicast path saturates well below
-// the P2P TMA kernel (0.79) on this box.
-int nvls_ctas() {
-    static int v = 0;
-    if (v == 0) {
-        const char* e = getenv("DASO_NVLS_CTAS");
-        v = e ? atoi(e) : 296;
-        if (v < 1) v = 1;
-    }
-    return v;
-}
-
-template <int OPS, int WIRE>
-__global__ void __launch_bounds__(kPeerThreads) nvls_kernel(const PeerArgs pa) {
-    const int G = pa.G;
-    if (!start_barrier(pa, G)) return;           // 1. start barrier: every peer's g is complete
-    bool bad = false;
-    const int64_t n = pa.a.n;
-    const int64_t nch = n / kNV;
-    const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
-    for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
-        nvls_body<OPS, WIRE, kNV>(pa, c * kNV, bad);
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t i = nch * kNV + threadIdx.x; i < n; i += kPeerThreads) nvls_body<OPS, WIRE, 1>(pa, i, bad);
-    }
-    if (pa.a.flag != nullptr) {
-        const unsigned any = __ballot_sync(0xffffffffu, bad);
-        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
-    }
-    end_barrier(pa, G);                          // 3. end barrier: every peer's shard has landed
-}
-
-template <int OPS, int WIRE>
-int launch_nvls_t(const PeerArgs& pa, cudaStream_t s, int sms) {
-    const int64_t nch = pa.a.n / kNV;
-    int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
-    (void)sms;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, nvls_ctas()));
-    nvls_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
-    return int(cudaGetLastError());
-}
-
-template <int WIRE>
-int dispatch_nvls(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
-    switch (ops) {
-        case OP_UPDATE: return launch_nvls_t<OP_UPDATE, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_PACK: return launch_nvls_t<OP_UPDATE | OP_PACK, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_MERGE: return launch_nvls_t<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
-        case OP_UPDATE | OP_MERGE | OP_PACK: return launch_nvls_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
-        default: return int(cudaErrorInvalidValue);
-    }
-}
-
 }  // namespace
-
-int launch_nvls(int ops, int wire, const PeerArgs& pa, void* stream) {
-    if (pa.G < 1 || pa.G > kMaxPeers || !pa.x_mc || !pa.g_mc) return int(cudaErrorInvalidValue);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (wire == DASO_WIRE_BF16) return dispatch_nvls<DASO_WIRE_BF16>(ops, pa, s, sms);
-    if (wire == DASO_WIRE_FP32) return dispatch_nvls<DASO_WIRE_FP32>(ops, pa, s, sms);
-    return int(cudaErrorInvalidValue);
-}
 
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream) {
     if (pa.G < 1 || pa.G > kMaxPeers) return int(cudaErrorInvalidValue);

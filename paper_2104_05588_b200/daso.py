@@ -15,7 +15,7 @@ from . import _lib as L
 from ._lib import DasoError, Record, check, lib  # noqa: F401
 
 WIRES = {"bf16": L.WIRE_BF16, "fp32": L.WIRE_FP32}
-MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED, "nvls": L.MODE_NVLS}
+MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED}
 
 
 def _torch():
@@ -143,7 +143,7 @@ class Ctx:
         self._check(lib().daso_bind(self._h, _ptr(x), _ptr(g), _ptr(v), n), "daso_bind")
 
     def alloc_bind(self, n: int):
-        """daso_alloc_bind: library-owned buckets (required by the "nvls" mode); returns torch
+        """daso_alloc_bind: library-owned (cudaMalloc) buckets; returns torch
         tensors x, g, v of daso_padded_numel(n, G) floats viewing them (valid until finalize)."""
         torch = _torch()
         px, pg, pv = C.c_void_p(), C.c_void_p(), C.c_void_p()
@@ -521,7 +521,7 @@ class FlatParams:
     def __init__(self, params, gpus_per_node: int = 1, align: int = 64, ctx: "Ctx | None" = None,
                  buckets=None):
         """ctx given: the buckets are allocated and bound by the library (daso_alloc_bind —
-        required for the "nvls" mode, and the fused mode's way around cuMem allocators);
+        the fused mode's way around cuMem allocators such as expandable_segments);
         buckets=(x, g, v) given: adopt existing (e.g. VCluster-owned) float32 buckets of
         >= n_pad elements; otherwise torch allocates them and the caller binds."""
         torch = _torch()

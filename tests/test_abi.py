@@ -90,6 +90,8 @@ def test_init_rejects_bad_epoch_config_and_enums():
     bad_wire = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, 7, L.MODE_FAITHFUL, 1, 0)
     assert L.lib().daso_init(C.byref(h), 2, 1, 4, 1, C.byref(bad_wire), C.c_char_p(b"\0" * 128)) == L.ERR_ARGUMENT
     assert L.lib().daso_init(None, 2, 1, 4, 1, C.byref(bad_wire), None) == L.ERR_ARGUMENT
+    bad_mode = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, L.WIRE_BF16, 3, 1, 0)
+    assert L.lib().daso_init(C.byref(h), 2, 1, 4, 1, C.byref(bad_mode), C.c_char_p(b"\0" * 128)) == L.ERR_ARGUMENT
 
 
 def test_kernel_entry_points_reject_bad_pointers_without_launching():
@@ -144,7 +146,8 @@ def test_bucket_partition_tiles_the_bucket():
 @pytest.mark.parametrize("world,G,mode,expect", [
     (4, 2, L.MODE_FAITHFUL, L.ERR_CONFIG),   # NCCL node collectives cannot loop back on one GPU
     (4, 2, L.MODE_SHARDED, L.ERR_CONFIG),
-    (4, 2, L.MODE_NVLS, L.ERR_CONFIG),
+    (4, 2, 3, L.ERR_CONFIG),                # not a fused mode at G > 1 (mode 3 no longer exists)
+    (2, 1, 3, L.ERR_ARGUMENT),              # no mode 3: the round-1 NVLS variant was removed
     (4, 3, L.MODE_FUSED, L.ERR_CONFIG),      # world % G != 0
     (18, 9, L.MODE_FUSED, L.ERR_CONFIG),     # G > 8 peers
 ])

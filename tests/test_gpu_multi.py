@@ -115,7 +115,7 @@ def test_world1_is_plain_sgd(tmp_path, mode):
 
 @pytest.mark.parametrize("P,G", [(2, 1), (1, 2)])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
-@pytest.mark.parametrize("mode", ["faithful", "fused", "nvls"])
+@pytest.mark.parametrize("mode", ["faithful", "fused"])
 def test_world2_toy(tmp_path, P, G, wire, mode):
     ranks = run_world(str(tmp_path), 2, TOY + ["--P", str(P), "--G", str(G), "--wire", wire, "--mode", mode])
     check(ranks, P, G, 4, 1, wire=wire)
@@ -133,8 +133,7 @@ def test_world2_S_equals_B(tmp_path):
     check(ranks, 2, 1, 2, 2, wire="fp32")
 
 
-@pytest.mark.parametrize("P,G,mode", [(2, 1, "faithful"), (2, 2, "faithful"), (2, 2, "sharded"), (2, 2, "fused"),
-                                      (2, 2, "nvls")])
+@pytest.mark.parametrize("P,G,mode", [(2, 1, "faithful"), (2, 2, "faithful"), (2, 2, "sharded"), (2, 2, "fused")])
 def test_blocking_fp32_is_flat_sync(tmp_path, P, G, mode):
     """B=1, S=0, fp32 wire: DASO == synchronous SGD over the concatenated batch."""
     ranks = run_world(str(tmp_path), P * G, ["--P", str(P), "--G", str(G), "--B", "1", "--S", "0", "--wire", "fp32",
@@ -144,7 +143,7 @@ def test_blocking_fp32_is_flat_sync(tmp_path, P, G, mode):
         np.testing.assert_array_equal(r["cks"], ranks[0]["cks"])   # blocking: all ranks identical
 
 
-@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused", "nvls"])
+@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused"])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
 def test_world4_toy_config1(tmp_path, mode, wire):
     """Config 1 proper: 2 virtual nodes x 2 GPUs, B=4, S=1, 20 steps."""
@@ -160,13 +159,15 @@ def test_world4_split_api_equals_step(tmp_path):
 
 
 @pytest.mark.parametrize("P,G", [(4, 1), (1, 4)])
-@pytest.mark.parametrize("mode", ["faithful", "fused", "nvls"])
+@pytest.mark.parametrize("mode", ["faithful", "fused", "fused-alloc"])
 def test_world4_other_topologies(tmp_path, P, G, mode):
-    ranks = run_world(str(tmp_path), 4, TOY + ["--P", str(P), "--G", str(G), "--mode", mode])
+    """fused-alloc: the fused mode on library-owned buckets (daso_alloc_bind, cudaMalloc)."""
+    extra = ["--mode", "fused", "--alloc"] if mode == "fused-alloc" else ["--mode", mode]
+    ranks = run_world(str(tmp_path), 4, TOY + ["--P", str(P), "--G", str(G), *extra])
     check(ranks, P, G, 4, 1)
 
 
-@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused", "nvls"])
+@pytest.mark.parametrize("mode", ["faithful", "sharded", "fused"])
 def test_world4_full_schedule(tmp_path, mode):
     args = ["--P", "2", "--G", "2", "--B", "4", "--S", "1", "--warmup", "1", "--cooldown", "1", "--epochs", "5",
             "--spe", "8", "--steps", "40", "--flags", "01100", "--mode", mode]
@@ -223,7 +224,7 @@ def test_backward_overlapped_local_sync(tmp_path, world, G):
 
 
 @pytest.mark.parametrize("mode,wire", [("fused", "bf16"), ("faithful", "bf16"), ("sharded", "bf16"),
-                                       ("fused", "fp32"), ("nvls", "bf16"), ("nvls", "fp32")])
+                                       ("fused", "fp32")])
 def test_full_size_microbench_sampled(tmp_path, mode, wire):
     """Full BASELINE size (n = 25,557,032, 2x2, B=4, S=1, bf16 wire), bench.py's launch
     configuration, 8 steps (two merges): 20,004 sampled parameters of every rank against

@@ -66,18 +66,22 @@ def test_vcluster_toy_config1(P, G, wire):
 
 @pytest.mark.parametrize("P,G", [(2, 2), (1, 4), (2, 4), (4, 2)])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
-def test_vcluster_tma_equals_register_path(P, G, wire):
-    """d = 40,000: shards of 2,500..20,000 span several 2048-parameter TMA tiles plus a ragged
-    tail; the TMA-staged fused kernel is bit-identical to the register path and both match
-    the oracle."""
+def test_vcluster_peer_data_paths_bit_identical(P, G, wire):
+    """d = 40,000: shards of 10,000..20,000 span several 2048-parameter tiles plus a ragged tail.
+    The fused node-tier kernel's three data paths — register (128-bit LDG/STG on peer
+    addresses), TMA-staged (one thread issues bulk copies between CTA barriers) and
+    warp-specialised TMA (the default: a driver warp and compute warps decoupled by mbarriers)
+    — compute the same arithmetic in the same order: bitwise equal, and all match the oracle."""
     kw = dict(steps=10, d=40000, wire=wire)
-    a, ra = run_vc(P, G, 4, 1, kernel="ldg", **kw)
-    b, rb = run_vc(P, G, 4, 1, kernel="tma", **kw)
-    for r in range(P * G):
-        for k in range(10):
-            np.testing.assert_array_equal(a[r][k].view(np.uint32), b[r][k].view(np.uint32))
-    assert ra == rb
-    check_trajectory(b, rb, toy_oracle(P, G, 4, 1, steps=10, d=40000, wire=wire), P, G, wire)
+    runs = {k: run_vc(P, G, 4, 1, kernel=k, **kw) for k in ("ldg", "tma", "auto")}
+    a, ra = runs["ldg"]
+    for k in ("tma", "auto"):
+        b, rb = runs[k]
+        for r in range(P * G):
+            for t in range(10):
+                np.testing.assert_array_equal(a[r][t].view(np.uint32), b[r][t].view(np.uint32))
+        assert ra == rb
+    check_trajectory(a, ra, toy_oracle(P, G, 4, 1, steps=10, d=40000, wire=wire), P, G, wire)
 
 
 @pytest.mark.parametrize("P,G", [(2, 4), (4, 2), (8, 1), (2, 2)])

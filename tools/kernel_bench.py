@@ -50,6 +50,7 @@ def main():
                                                                          pack_out=pk), 20 + (P + 1) * wb),
         "K3_update_merge_P8": (lambda: daso.daso_k_update_merge(x, v, g, 1e-3, 0.9, 1e-4, 0.5, slot[:8], 1), 20 + 8 * wb),
         f"K4_average_P{P}": (lambda: daso.daso_k_average(x, slot[:P]), P * wb + 4),
+        "K4_average_P4": (lambda: daso.daso_k_average(x, slot[:4]), 4 * wb + 4),
         "pack_only": (lambda: daso.daso_k_pack(x, pk), 4 + wb),
     }
     xs = x[:n]
