@@ -483,6 +483,11 @@ def run_ours(a):
                     "bytes_per_launch": nvl_bytes, "bytes_def": "NVLink bytes per direction per GPU",
                     "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1),
                     "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
+                    "probe_ceiling_gbs": 660.0,
+                    "frac_of_probe_ceiling": nvl_gbs / 660.0,
+                    "probe": "tools/nvlink_kernels.cu tma_rw: this kernel's NVLink traffic pattern with no arithmetic, "
+                             "no local x/v traffic and no barriers reaches 0.857 x 770 = 660 GB/s per direction at "
+                             "G = 2 and 4 (profiles/r02/multi4_a/nvk_g*.jsonl)",
                     "hbm": roofline}
     phases = {k: (tr[k] / a.steps if k.endswith("_ms") else tr[k]) for k in tr}
     if tr["local_ms"] > 0:

@@ -36,10 +36,14 @@ def run(overlap, rank, world, G, uid, steps):
                          wire="fp32")
     ctx.bind(flat.x, flat.g, flat.v, flat.n)
     rec = torch.zeros_like(flat.g)
+
+    def recorder(o, k):
+        def hook(_p):
+            rec[o:o + k].copy_(flat.g[o:o + k])
+        return hook
     # recording hooks first: they run before OverlappedLocalSync's hook of the same parameter
     for p, o in zip(flat.params, flat.offsets):
-        p.register_post_accumulate_grad_hook(
-            lambda _p, o=o, k=p.numel(): rec[o:o + k].copy_(flat.g[o:o + k]))
+        p.register_post_accumulate_grad_hook(recorder(o, p.numel()))
     ov = daso.OverlappedLocalSync(ctx, flat, bucket_mb=0.05) if overlap else None
     gen = torch.Generator(device=dev).manual_seed(100 + rank)
     trace, grads = [], []
