@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--nccl-max-ctas", type=int, default=0, help="cap the side-stream exchange's NCCL CTAs")
+    ap.add_argument("--exchange", choices=["nccl", "ce"], default="nccl",
+                    help="global-tier transport: NCCL all-gather or copy-engine pushes (DASO_EXCH_CE)")
     ap.add_argument("--compute-ms", type=float, default=0.0,
                     help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
                          "the global exchange the next batch's compute hides")
@@ -402,7 +404,7 @@ def run_ours(a):
     uid = daso.rendezvous_unique_id() if world > 1 else daso.daso_get_unique_id()
     ctx = daso.daso_init(world, G, a.B, a.S, rank=rank, uid=uid, total_epochs=1,
                          steps_per_epoch=a.B * (1 << 20), momentum=0.9, weight_decay=1e-4, wire=a.wire,
-                         mode=a.mode, nccl_max_ctas=a.nccl_max_ctas)
+                         mode=a.mode, nccl_max_ctas=a.nccl_max_ctas, exchange=a.exchange)
     n_pad = daso.daso_padded_numel(n, G)
     x = torch.zeros(n_pad, dtype=torch.float32, device=dev)
     g = torch.zeros_like(x)
@@ -551,7 +553,7 @@ def run_ours(a):
             "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "sync-path microbench (config 2): n=25,557,032 fp32 params, synthetic grads",
-                       "n_params": n, "topology": f"{P}x{G}", "B": a.B, "S": a.S, "mode": a.mode,
+                       "n_params": n, "topology": f"{P}x{G}", "B": a.B, "S": a.S, "mode": a.mode, "exchange": a.exchange,
                        "wire": a.wire, "parallelism": f"daso {P} virtual nodes x {G} GPUs",
                        "l2": "flushed before every timed step (untimed read of a 256 MB buffer after the "
                              "gradient refresh); the inputs (x, v, g = 307 MB) also exceed the 126 MB L2",

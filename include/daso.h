@@ -135,7 +135,12 @@ typedef struct {
     int32_t mode;             /* DASO_MODE_FAITHFUL / _SHARDED / _FUSED (see the enum above) */
     int32_t check_finite;     /* 1 = fused non-finite flag in every update kernel */
     int32_t nccl_max_ctas;    /* >0: cap NCCL CTAs on the group (side-stream) comm to leave SMs to compute; 0 = NCCL default */
+    int32_t exchange;         /* global-tier transport: DASO_EXCH_NCCL = in-place ncclAllGather on the
+                                 group comm (side stream); DASO_EXCH_CE = copy-engine pushes into the group members'
+                                 CUDA-IPC-mapped slots + stream memory-op flags, no SMs used */
 } daso_config;
+
+enum { DASO_EXCH_NCCL = 0, DASO_EXCH_CE = 1 };
 
 /* Fill `out` (128 bytes) with a fresh NCCL unique id.  Call on rank 0 only and
  * broadcast the bytes to every rank (torch.distributed does this in the binding). */

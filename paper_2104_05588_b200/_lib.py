@@ -18,6 +18,7 @@ WARMUP, CYCLING, COOLDOWN = 0, 1, 2
 WIRE_BF16, WIRE_FP32 = 0, 1
 MODE_FAITHFUL, MODE_SHARDED, MODE_FUSED = 0, 1, 2
 STEP_GRADS_REDUCED = 1
+EXCH_NCCL, EXCH_CE = 0, 1
 
 
 class SchedConfig(C.Structure):
@@ -42,7 +43,7 @@ class Config(C.Structure):
     _fields_ = [("rank", C.c_int32), ("warmup_epochs", C.c_int32), ("cooldown_epochs", C.c_int32),
                 ("total_epochs", C.c_int32), ("steps_per_epoch", C.c_int32), ("momentum", C.c_float),
                 ("weight_decay", C.c_float), ("wire", C.c_int32), ("mode", C.c_int32),
-                ("check_finite", C.c_int32), ("nccl_max_ctas", C.c_int32)]
+                ("check_finite", C.c_int32), ("nccl_max_ctas", C.c_int32), ("exchange", C.c_int32)]
 
 
 TRACE_FIELDS = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("kernel_ms", C.c_double),

@@ -51,6 +51,19 @@ struct daso_ctx {
     int infl_group = -1, infl_S = 0;
     bool exch_enabled = true;   // daso_set_exchange(0): timing knob, the group all-gather is skipped
 
+    // copy-engine group exchange (cfg.exchange == DASO_EXCH_CE): every member pushes its packed row
+    // into row `node` of every group member's slot with cudaMemcpyAsync (copy engines over NVLink,
+    // CUDA IPC mappings), then raises a flag there with cuStreamWriteValue64; receivers wait with
+    // cuStreamWaitValue64.  xs = own [2P] u64: [0,P) epoch of the last row received from member i,
+    // [P,2P) epoch of the last exchange member i has consumed (merged / averaged) — flow control
+    // before a row of i's slot is overwritten.
+    bool ce = false;
+    std::vector<void*> peer_slot;                 // [P] group members' slot bases (own = slot)
+    std::vector<unsigned long long*> peer_xs;     // [P] group members' xs arrays
+    unsigned long long* xs = nullptr;
+    unsigned long long exch_epoch = 0;            // exchanges this rank has issued
+    std::vector<void*> ipc_group;                 // opened group mappings
+
     // fused mode: node peers' buffers mapped through CUDA IPC (NVLink peer memory)
     float* peer_x[daso::kMaxPeers] = {};
     float* peer_g[daso::kMaxPeers] = {};
@@ -207,6 +220,39 @@ int launch(daso_ctx* c, int ops, const daso::KernelArgs& a, cudaStream_t s) {
     return daso::launch_fused(ops, c->cfg.wire, a, s);
 }
 
+// ---- stream memory operations (driver API, resolved at run time) -----------------------
+typedef CUresult (*PfnWriteValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PfnWaitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PfnDevAttr)(int*, CUdevice_attribute, CUdevice);
+
+template <typename F>
+F driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<F>(p);
+    return nullptr;
+}
+PfnWriteValue64 write_value64() {
+    static PfnWriteValue64 f = driver_fn<PfnWriteValue64>("cuStreamWriteValue64");
+    return f;
+}
+PfnWaitValue64 wait_value64() {
+    static PfnWaitValue64 f = driver_fn<PfnWaitValue64>("cuStreamWaitValue64");
+    return f;
+}
+int wait_flags(int device) {   // GEQ, plus a flush of remote writes where the device supports it
+    static int flags = -1;
+    if (flags < 0) {
+        flags = CU_STREAM_WAIT_VALUE_GEQ;
+        PfnDevAttr attr = driver_fn<PfnDevAttr>("cuDeviceGetAttribute");
+        int can = 0;
+        if (attr && attr(&can, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, CUdevice(device)) == CUDA_SUCCESS && can)
+            flags |= CU_STREAM_WAIT_VALUE_FLUSH;
+    }
+    return flags;
+}
+
 // ---- collectives ---------------------------------------------------------------
 // Non-blocking global exchange: after the packing kernel on the compute
 // stream, the side stream runs the in-place group all-gather of the slot.
@@ -217,7 +263,25 @@ daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
     }
     CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
-    if (c->exch_enabled) {
+    if (c->ce) {   // copy-engine pushes into every group member's slot (no SMs)
+        const unsigned long long e = ++c->exch_epoch;
+        const size_t row = size_t(c->seg) * c->wire_bytes;
+        Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(row));
+        for (int k = 1; k < c->P && c->exch_enabled; ++k) {
+            const int i = (c->node + k) % c->P;             // start with the next member: spread the links
+            // member i has consumed exchange e-1, so row `node` of its slot is free
+            if (wait_value64()(c->side, CUdeviceptr(c->xs + c->P + i), e - 1, wait_flags(c->device)) != CUDA_SUCCESS)
+                return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange flow control) failed");
+            CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row, own_segment(c),
+                                        row, cudaMemcpyDeviceToDevice, c->side));
+            if (write_value64()(c->side, CUdeviceptr(c->peer_xs[i] + c->node), e, 0) != CUDA_SUCCESS)
+                return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange flag) failed");
+        }
+        if (!c->exch_enabled)   // timing knob: flags only, no data
+            for (int i = 0; i < c->P; ++i)
+                if (i != c->node && write_value64()(c->side, CUdeviceptr(c->peer_xs[i] + c->node), e, 0) != CUDA_SUCCESS)
+                    return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange flag) failed");
+    } else if (c->exch_enabled) {
         Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(c->seg) * double(c->wire_bytes));
         NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
                                   c->side));
@@ -229,7 +293,22 @@ daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
 daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
     if (c->vc) return DASO_OK;   // virtual cluster: the loopback copies precede on the same stream
     Span sp(c, s, PH_WAIT, 0.0);
-    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));   // own outgoing copies / all-gather done
+    if (c->ce)   // every other member's row of this exchange has landed in the slot
+        for (int i = 0; i < c->P; ++i)
+            if (i != c->node &&
+                wait_value64()(s, CUdeviceptr(c->xs + i), c->exch_epoch, wait_flags(c->device)) != CUDA_SUCCESS)
+                return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange arrival) failed");
+    return DASO_OK;
+}
+
+// The slot rows of the current exchange have been read (merge / blocking average issued on s):
+// tell every member its row in this rank's slot may be overwritten (copy-engine exchange only).
+daso_status exchange_consumed(daso_ctx* c, cudaStream_t s) {
+    if (!c->ce || c->vc) return DASO_OK;
+    for (int i = 0; i < c->P; ++i)
+        if (i != c->node && write_value64()(s, CUdeviceptr(c->peer_xs[i] + c->P + c->node), c->exch_epoch, 0) != CUDA_SUCCESS)
+            return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange ack) failed");
     return DASO_OK;
 }
 
@@ -250,6 +329,7 @@ daso_status faithful_blocking_tail(daso_ctx* c, int group, cudaStream_t s) {
         daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
         av.den = float(c->P);
         KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+        STATUS_TRY(exchange_consumed(c, s));
     }
     return node_bcast(c, group, s);
 }
@@ -260,7 +340,7 @@ daso_status shard_blocking_tail(daso_ctx* c, cudaStream_t s) {   // sharded / fu
     daso::KernelArgs av = base_args(c, off, c->seg, 0.f);
     av.den = float(c->P);
     KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
-    return DASO_OK;
+    return exchange_consumed(c, s);
 }
 
 daso_status fused_blocking_tail(daso_ctx* c, cudaStream_t s) {
@@ -314,6 +394,7 @@ daso_status step_faithful(daso_ctx* c, const daso_record& r, float lr, cudaStrea
         a.pack_out = own_segment(c);
     }
     KERN_TRY(c, launch(c, ops, a, s));
+    if (merge_here) STATUS_TRY(exchange_consumed(c, s));
     if (merge) {
         STATUS_TRY(node_bcast(c, int(r.merge_group), s));
         c->inflight = false;
@@ -369,6 +450,7 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
         a.pack_out = own_segment(c);
     }
     KERN_TRY(c, launch(c, ops, a, s));
+    if (merge) STATUS_TRY(exchange_consumed(c, s));
     if (send) {
         STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {
@@ -444,6 +526,7 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
         Span sp(c, s, PH_KERNEL, per * double(sh));
         KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
     }
+    if (merge) STATUS_TRY(exchange_consumed(c, s));
     if (send) {
         STATUS_TRY(start_exchange(c, s));
         if (r.blocking) {
@@ -536,6 +619,55 @@ daso_status setup_peers(daso_ctx* c) {
     return DASO_OK;
 }
 
+// Copy-engine group exchange: map every group member's slot and flag array (CUDA IPC handles
+// exchanged over the group communicator at bind time).
+struct GroupExport {
+    cudaIpcMemHandle_t slot, xs;
+};
+
+daso_status setup_group_ce(daso_ctx* c) {
+    PfnDevAttr attr = driver_fn<PfnDevAttr>("cuDeviceGetAttribute");
+    int can = 0;
+    if (!write_value64() || !wait_value64() || !attr ||
+        attr(&can, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, CUdevice(c->device)) != CUDA_SUCCESS || !can)
+        return c->fail(DASO_ERR_CONFIG, "DASO_EXCH_CE needs 64-bit stream memory operations (cuStreamWaitValue64)");
+    const size_t xs_bytes = (2 * size_t(c->P) + 1) * sizeof(unsigned long long);   // + barrier scratch
+    CUDA_TRY(c, cudaMalloc(&c->xs, xs_bytes));
+    CUDA_TRY(c, cudaMemset(c->xs, 0, xs_bytes));
+    GroupExport mine{};
+    CUDA_TRY(c, cudaIpcGetMemHandle(&mine.slot, c->slot));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&mine.xs, c->xs));
+    std::vector<GroupExport> all(c->P);
+    void* dbuf = nullptr;
+    CUDA_TRY(c, cudaMalloc(&dbuf, sizeof(GroupExport) * c->P));
+    CUDA_TRY(c, cudaMemcpy(static_cast<char*>(dbuf) + sizeof(GroupExport) * c->node, &mine, sizeof mine,
+                           cudaMemcpyHostToDevice));
+    NCCL_TRY(c, ncclAllGather(static_cast<char*>(dbuf) + sizeof(GroupExport) * c->node, dbuf, sizeof(GroupExport),
+                              ncclUint8, c->group_comm, c->side));
+    CUDA_TRY(c, cudaStreamSynchronize(c->side));
+    CUDA_TRY(c, cudaMemcpy(all.data(), dbuf, sizeof(GroupExport) * c->P, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    c->peer_slot.assign(size_t(c->P), nullptr);
+    c->peer_xs.assign(size_t(c->P), nullptr);
+    for (int i = 0; i < c->P; ++i) {
+        if (i == c->node) {
+            c->peer_slot[i] = c->slot;
+            c->peer_xs[i] = c->xs;
+            continue;
+        }
+        void* ms = nullptr;
+        void* mx = nullptr;
+        CUDA_TRY(c, cudaIpcOpenMemHandle(&ms, all[i].slot, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_group.push_back(ms);
+        CUDA_TRY(c, cudaIpcOpenMemHandle(&mx, all[i].xs, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_group.push_back(mx);
+        c->peer_slot[i] = ms;
+        c->peer_xs[i] = static_cast<unsigned long long*>(mx);
+    }
+    c->ce = true;
+    return DASO_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -581,6 +713,7 @@ daso_status make_ctx(daso_ctx** out, int world, int gpus_per_node, int B, int S,
     if (world < 1 || gpus_per_node < 1 || world % gpus_per_node != 0 || B < 1) return DASO_ERR_CONFIG;
     if (cfg->rank < 0 || cfg->rank >= world) return DASO_ERR_RANGE;
     if (cfg->wire != DASO_WIRE_BF16 && cfg->wire != DASO_WIRE_FP32) return DASO_ERR_ARGUMENT;
+    if (cfg->exchange != DASO_EXCH_NCCL && cfg->exchange != DASO_EXCH_CE) return DASO_ERR_ARGUMENT;
     if (cfg->mode != DASO_MODE_FAITHFUL && cfg->mode != DASO_MODE_SHARDED && cfg->mode != DASO_MODE_FUSED)
         return DASO_ERR_ARGUMENT;
     if (cfg->mode == DASO_MODE_FUSED && gpus_per_node > daso::kMaxPeers)
@@ -696,6 +829,7 @@ daso_status bind_impl(daso_ctx* c, float* x, float* g, float* v, size_t n) {
         CUDA_TRY(c, cudaMemset(c->slot, 0, bytes));
     }
     if (c->cfg.mode == DASO_MODE_FUSED && c->G > 1 && !c->vc) STATUS_TRY(setup_peers(c));
+    if (c->cfg.exchange == DASO_EXCH_CE && c->P > 1 && !c->vc) STATUS_TRY(setup_group_ce(c));
     CUDA_TRY(c, cudaDeviceSynchronize());
     c->bound = true;
     return DASO_OK;
@@ -744,6 +878,7 @@ daso_status daso_global_send(daso_ctx* c, int group, int S, void* stream) {
             daso::KernelArgs av = base_args(c, 0, c->n, 0.f);
             av.den = float(c->P);
             KERN_TRY(c, launch(c, daso::OP_AVERAGE, av, s));
+            STATUS_TRY(exchange_consumed(c, s));
         }
         STATUS_TRY(node_bcast(c, group, s));
     } else {
@@ -765,6 +900,7 @@ daso_status daso_global_merge(daso_ctx* c, void* stream) {
         daso::KernelArgs m = base_args(c, 0, c->n, 0.f);
         m.den = float(2 * c->infl_S + c->P);
         KERN_TRY(c, launch(c, daso::OP_MERGE, m, s));
+        STATUS_TRY(exchange_consumed(c, s));
     }
     STATUS_TRY(node_bcast(c, c->infl_group, s));
     c->inflight = false;
@@ -898,11 +1034,27 @@ daso_status daso_exchange_alone(daso_ctx* c, int iters, double* ms_out) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     CUDA_TRY(c, cudaEventCreate(&e0));
     CUDA_TRY(c, cudaEventCreate(&e1));
-    NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm, c->side));
+    const size_t row = size_t(c->seg) * c->wire_bytes;
+    auto one = [&]() -> daso_status {
+        if (!c->ce) {
+            NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
+                                      c->side));
+            return DASO_OK;
+        }
+        for (int k = 1; k < c->P; ++k) {   // the copy-engine pushes of one exchange, no flags
+            const int i = (c->node + k) % c->P;
+            CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row, own_segment(c),
+                                        row, cudaMemcpyDeviceToDevice, c->side));
+        }
+        return DASO_OK;
+    };
+    if (c->ce) {   // align the members: nobody starts pushing before everybody is idle
+        unsigned long long* scratch = c->xs + 2 * c->P;
+        NCCL_TRY(c, ncclAllReduce(scratch, scratch, 1, ncclUint64, ncclSum, c->group_comm, c->side));
+    }
+    STATUS_TRY(one());
     CUDA_TRY(c, cudaEventRecord(e0, c->side));
-    for (int i = 0; i < iters; ++i)
-        NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
-                                  c->side));
+    for (int i = 0; i < iters; ++i) STATUS_TRY(one());
     CUDA_TRY(c, cudaEventRecord(e1, c->side));
     CUDA_TRY(c, cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -926,6 +1078,16 @@ daso_status daso_finalize(daso_ctx* c) {
         }
         for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
         if (c->sig) cudaFree(c->sig);
+    }
+    if (!c->ipc_group.empty() || c->xs) {
+        // no group member may still push into this rank's slot: group barrier before unmapping
+        if (c->group_comm && c->xs && c->side) {
+            unsigned long long* scratch = c->xs + 2 * c->P;
+            ncclAllReduce(scratch, scratch, 1, ncclUint64, ncclSum, c->group_comm, c->side);
+            cudaStreamSynchronize(c->side);
+        }
+        for (void* p : c->ipc_group) cudaIpcCloseMemHandle(p);
+        if (c->xs) cudaFree(c->xs);
     }
     cudaDeviceSynchronize();
     for (int b = 0; b < 3; ++b)

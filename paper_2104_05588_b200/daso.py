@@ -15,6 +15,7 @@ from . import _lib as L
 from ._lib import DasoError, Record, check, lib  # noqa: F401
 
 WIRES = {"bf16": L.WIRE_BF16, "fp32": L.WIRE_FP32}
+EXCHANGES = {"nccl": L.EXCH_NCCL, "ce": L.EXCH_CE}
 MODES = {"faithful": L.MODE_FAITHFUL, "sharded": L.MODE_SHARDED, "fused": L.MODE_FUSED}
 
 
@@ -234,9 +235,9 @@ def daso_init(world: int, gpus_per_node: int, B: int, S: int, *, rank: int, uid:
               warmup_epochs: int = 0, cooldown_epochs: int = 0, total_epochs: int = 1,
               steps_per_epoch: int = 1 << 20, momentum: float = 0.9, weight_decay: float = 1e-4,
               wire: str = "bf16", mode: str = "faithful", check_finite: bool = True,
-              nccl_max_ctas: int = 0) -> Ctx:
+              nccl_max_ctas: int = 0, exchange: str = "nccl") -> Ctx:
     cfg = _config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay, wire,
-                  mode, check_finite, nccl_max_ctas)
+                  mode, check_finite, nccl_max_ctas, exchange)
     if len(uid) != 128:
         raise ValueError("uid must be 128 bytes")
     h = C.c_void_p()
@@ -250,9 +251,9 @@ def daso_init(world: int, gpus_per_node: int, B: int, S: int, *, rank: int, uid:
 
 
 def _config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay, wire, mode,
-            check_finite, nccl_max_ctas) -> L.Config:
+            check_finite, nccl_max_ctas, exchange="nccl") -> L.Config:
     return L.Config(rank, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay,
-                    WIRES[wire], MODES[mode], int(check_finite), nccl_max_ctas)
+                    WIRES[wire], MODES[mode], int(check_finite), nccl_max_ctas, EXCHANGES[exchange])
 
 
 class VCluster:

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--mode", default="fused")
     ap.add_argument("--wire", default="bf16")
+    ap.add_argument("--exchange", default="nccl")
     ap.add_argument("--alloc", action="store_true", help="daso_alloc_bind instead of torch buckets")
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
@@ -40,7 +41,7 @@ def main():
     dist.init_process_group("gloo")
     uid = daso.rendezvous_unique_id()
     ctx = daso.daso_init(world, a.G, 4, 1, rank=rank, uid=uid, total_epochs=1, steps_per_epoch=4 << 20,
-                         momentum=0.9, weight_decay=1e-4, wire=a.wire, mode=a.mode)
+                         momentum=0.9, weight_decay=1e-4, wire=a.wire, mode=a.mode, exchange=a.exchange)
     n_pad = daso.daso_padded_numel(N, a.G)
     if a.alloc:                                   # library-owned (cudaMalloc) buckets
         x, g, v = ctx.alloc_bind(N)

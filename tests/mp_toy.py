@@ -42,6 +42,7 @@ def parse(argv=None):
     ap.add_argument("--mode", default="faithful")
     ap.add_argument("--split", action="store_true", help="drive the split API instead of daso_step")
     ap.add_argument("--kernel", default="", help="ldg | tma: fused-kernel data path (daso_kernel_impl)")
+    ap.add_argument("--exchange", default="nccl", help="nccl | ce (copy-engine group exchange)")
     ap.add_argument("--alloc", action="store_true", help="daso_alloc_bind instead of torch buckets")
     ap.add_argument("--out", required=True)
     return ap.parse_args(argv)
@@ -61,7 +62,7 @@ def run_toy(a, rank: int = 0, world: int = 1, uid: bytes | None = None):
     uid = uid if uid is not None else daso.daso_get_unique_id()
     ctx = daso.daso_init(world, a.G, a.B, a.S, rank=rank, uid=uid, warmup_epochs=a.warmup,
                          cooldown_epochs=a.cooldown, total_epochs=a.epochs, steps_per_epoch=a.spe,
-                         momentum=a.mu, weight_decay=a.wd, wire=a.wire, mode=a.mode)
+                         momentum=a.mu, weight_decay=a.wd, wire=a.wire, mode=a.mode, exchange=a.exchange)
     n_pad = daso.daso_padded_numel(a.d, a.G)
     if a.alloc:                                                   # library-owned (cudaMalloc) buckets
         x, g, v = ctx.alloc_bind(a.d)                             # zeroed: x0 = 0 on every rank (R17)

@@ -90,6 +90,8 @@ def test_init_rejects_bad_epoch_config_and_enums():
     bad_wire = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, 7, L.MODE_FAITHFUL, 1, 0)
     assert L.lib().daso_init(C.byref(h), 2, 1, 4, 1, C.byref(bad_wire), C.c_char_p(b"\0" * 128)) == L.ERR_ARGUMENT
     assert L.lib().daso_init(None, 2, 1, 4, 1, C.byref(bad_wire), None) == L.ERR_ARGUMENT
+    bad_exch = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, L.WIRE_BF16, L.MODE_FUSED, 1, 0, 2)
+    assert L.lib().daso_init(C.byref(h), 2, 1, 4, 1, C.byref(bad_exch), C.c_char_p(b"\0" * 128)) == L.ERR_ARGUMENT
     bad_mode = L.Config(0, 0, 0, 1, 64, 0.9, 1e-4, L.WIRE_BF16, 3, 1, 0)
     assert L.lib().daso_init(C.byref(h), 2, 1, 4, 1, C.byref(bad_mode), C.c_char_p(b"\0" * 128)) == L.ERR_ARGUMENT
 

@@ -223,9 +223,10 @@ def test_backward_overlapped_local_sync(tmp_path, world, G):
             np.testing.assert_array_equal(fs[i]["overlap"].view(np.uint32), fs[i]["plain"].view(np.uint32))
 
 
-@pytest.mark.parametrize("mode,wire", [("fused", "bf16"), ("faithful", "bf16"), ("sharded", "bf16"),
-                                       ("fused", "fp32")])
-def test_full_size_microbench_sampled(tmp_path, mode, wire):
+@pytest.mark.parametrize("mode,wire,exchange", [("fused", "bf16", "nccl"), ("faithful", "bf16", "nccl"),
+                                                ("sharded", "bf16", "nccl"), ("fused", "fp32", "nccl"),
+                                                ("fused", "bf16", "ce")])
+def test_full_size_microbench_sampled(tmp_path, mode, wire, exchange):
     """Full BASELINE size (n = 25,557,032, 2x2, B=4, S=1, bf16 wire), bench.py's launch
     configuration, 8 steps (two merges): 20,004 sampled parameters of every rank against
     the oracle simulating exactly those elements (the method is elementwise given the
@@ -235,7 +236,8 @@ def test_full_size_microbench_sampled(tmp_path, mode, wire):
     sys.path.insert(0, HERE)
     import mp_micro
     out = str(tmp_path / "out")
-    torchrun(4, "mp_micro.py", ["--G", "2", "--mode", mode, "--wire", wire, "--out", out], timeout=900)
+    torchrun(4, "mp_micro.py", ["--G", "2", "--mode", mode, "--wire", wire, "--exchange", exchange, "--out", out],
+             timeout=900)
     idx = mp_micro.sample_indices()
     N = mp_micro.N
     grads = {(rk, k): synthetic.microbench_grad(N, rk, k)[idx] for rk in range(4) for k in range(8)}
@@ -250,6 +252,22 @@ def test_full_size_microbench_sampled(tmp_path, mode, wire):
             rms = np.sqrt(np.mean(xo ** 2))
             assert np.all(np.abs(tr[k] - xo) <= tol * (np.abs(xo) + rms)), (rk, k)
             assert np.linalg.norm(tr[k] - xo) <= tol * np.linalg.norm(xo)
+
+
+@pytest.mark.parametrize("P,G,mode,wire", [(2, 1, "faithful", "bf16"), (2, 1, "fused", "fp32"), (2, 2, "fused", "bf16"),
+                                           (2, 2, "fused", "fp32"), (2, 2, "faithful", "bf16"), (4, 1, "fused", "bf16")])
+def test_copy_engine_exchange(tmp_path, P, G, mode, wire):
+    """DASO_EXCH_CE: the global tier as copy-engine pushes into the group members' IPC-mapped
+    slots + stream memory-op flags and acks, instead of NCCL's all-gather — the same records,
+    the same trajectory as the oracle (config 1, and the full warm-up / cycling / cool-down
+    schedule with its blocking syncs)."""
+    ranks = run_world(str(tmp_path / "a"), P * G, TOY + ["--P", str(P), "--G", str(G), "--mode", mode, "--wire", wire,
+                                                     "--exchange", "ce"])
+    check(ranks, P, G, 4, 1, wire=wire)
+    args = ["--P", str(P), "--G", str(G), "--B", "4", "--S", "1", "--warmup", "1", "--cooldown", "1", "--epochs", "5",
+            "--spe", "8", "--steps", "40", "--flags", "01100", "--mode", mode, "--wire", wire, "--exchange", "ce"]
+    ranks = run_world(str(tmp_path / "b"), P * G, args)
+    check(ranks, P, G, 4, 1, steps=40, warm=1, cool=1, epochs=5, spe=8, flags="01100", wire=wire)
 
 
 def test_config5_schedule_through_daso_step(tmp_path):
