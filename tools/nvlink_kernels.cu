@@ -15,7 +15,7 @@
 //   ce_bidi  : copy engines, every GPU copies (G-1)/G 4n to its peers (cudaMemcpyPeerAsync)
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/nvk tools/nvlink_kernels.cu
-//   /tmp/nvk [n_params] [ctas (0 = SMs-16)] [stages]
+//   /tmp/nvk [n_params] [ctas (0 = SMs-16)] [stages (0 = auto)] [tile floats (2048)]
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,7 +34,7 @@
         }                                                                                      \
     } while (0)
 
-constexpr int kMax = 8, kT = 2048, kThr = 256;
+constexpr int kMax = 8, kThr = 256;
 
 struct Args {
     const float* gp[kMax];   // every GPU's g at this GPU's shard
@@ -42,7 +42,7 @@ struct Args {
     float* rp[kMax];         // push: owner q's receive buffer, row `me`
     const float* gq[kMax];   // push: this GPU's g at shard q
     int64_t n;               // shard length
-    int G, me, NS;
+    int G, me, NS, T;        // T = tile (floats per bulk copy)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -50,7 +50,7 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return uint32_t(__cvta
 template <bool RD, bool WR>
 __global__ void __launch_bounds__(kThr, 1) tma_kernel(Args a) {
     extern __shared__ __align__(128) unsigned char sm[];
-    const int G = a.G, NS = a.NS;
+    const int G = a.G, NS = a.NS, kT = a.T;
     const uint32_t stage = uint32_t(G) * kT * 4;
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + size_t(NS) * stage);
     const int64_t nt = a.n / kT;
@@ -139,6 +139,7 @@ int main(int argc, char** argv) {
     const int64_t N = argc > 1 ? atoll(argv[1]) : 25557056;
     int ctas = argc > 2 ? atoi(argv[2]) : 0;
     const int NSreq = argc > 3 ? atoi(argv[3]) : 0;
+    const int kT = argc > 4 ? atoi(argv[4]) : 2048;
     const int64_t n = (N / G) / kT * kT;   // shard, whole tiles
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -157,6 +158,10 @@ int main(int argc, char** argv) {
     }
     const uint32_t stage = uint32_t(G) * kT * 4;
     const int NS = NSreq > 0 ? NSreq : int(std::min<int64_t>(8, (200 * 1024) / stage));
+    if (NS < 2) {
+        printf("{\"skip\": \"tile %d x G %d leaves < 2 stages\"}\n", kT, G);
+        return 0;
+    }
     const size_t smem = size_t(NS) * stage + 8 * NS;
     auto args = [&](int d) {
         Args a{};
@@ -170,6 +175,7 @@ int main(int argc, char** argv) {
         a.G = G;
         a.me = d;
         a.NS = NS;
+        a.T = kT;
         return a;
     };
     auto run = [&](const char* name, double bytes_dir, auto launch) {
@@ -206,9 +212,9 @@ int main(int argc, char** argv) {
             CK(cudaEventElapsedTime(&ms, e0[d], e1[d]));
             worst = std::max(worst, ms / iters);
         }
-        printf("{\"probe\": \"%s\", \"G\": %d, \"shard\": %lld, \"ctas\": %d, \"stages\": %d, \"us\": %.1f, "
-               "\"GBs_per_dir\": %.1f, \"frac_770\": %.3f}\n",
-               name, G, (long long)n, ctas, NS, worst * 1e3, bytes_dir / (worst * 1e-3) / 1e9,
+        printf("{\"probe\": \"%s\", \"G\": %d, \"shard\": %lld, \"ctas\": %d, \"stages\": %d, \"tile\": %d, "
+               "\"us\": %.1f, \"GBs_per_dir\": %.1f, \"frac_770\": %.3f}\n",
+               name, G, (long long)n, ctas, NS, kT, worst * 1e3, bytes_dir / (worst * 1e-3) / 1e9,
                bytes_dir / (worst * 1e-3) / 1e9 / 770.0);
         fflush(stdout);
     };
