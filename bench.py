@@ -70,6 +70,9 @@ def parse():
                     help="fwd/bwd stand-in per batch inside the hidden-fraction cycles (P > 1); config 3's "
                          "real fwd/bwd (~55 ms at 256/GPU) hides the exchange trivially but drowns it in noise")
     ap.add_argument("--cycles", type=int, default=30, help="B-cycles per leg of the hidden-fraction measurement")
+    ap.add_argument("--overlap-compute", choices=["gemm", "sleep", "both"], default="both",
+                    help="fwd/bwd stand-in of the hidden-fraction cycles: bf16 GEMMs (SM/HBM contention, jittery), "
+                         "a deterministic device sleep (precise), or both")
     ap.add_argument("--dump-steps", action="store_true", help="add every timed step's ms and kind to the line")
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline table (N=1)")
     ap.add_argument("--ref-div", type=int, default=4,
@@ -339,6 +342,24 @@ def make_compute_small(ms: float, dev):
     return run
 
 
+def make_sleep(ms: float):
+    """Deterministic fwd/bwd stand-in for the hidden-fraction cycles: one spinning thread
+    (torch.cuda._sleep) for ~ms of device time.  Unlike GEMMs it has no run-to-run jitter, so a
+    40-100 us exchange is resolvable; it does not model SM or HBM contention (the GEMM legs do)."""
+    if ms <= 0:
+        return lambda: None
+    import torch
+    torch.cuda._sleep(1000)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    torch.cuda._sleep(10_000_000)
+    e1.record()
+    torch.cuda.synchronize()
+    cycles = int(10_000_000 * ms / e0.elapsed_time(e1))
+    return lambda: torch.cuda._sleep(cycles)
+
+
 def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t_ag):
     """SURVEY §8(d) hidden fraction: hidden = 1 - (T_with - T_without) / T_AG,alone, per B-cycle.
     One cycle = B batches of [fwd/bwd stand-in (bf16 GEMMs) ; gradient refresh ; daso_step], timed by
@@ -510,8 +531,13 @@ def run_ours(a):
     overlap = None
     if P > 1:
         nx = 1 if a.S > 0 else a.B          # exchanges issued per B-cycle
-        overlap = overlap_cycles(ctx, a, g, g_src, stream, world, make_compute_small(a.overlap_compute_ms, dev), nx,
-                                 t_ag)
+        overlap = {}
+        if a.overlap_compute in ("sleep", "both"):
+            overlap["sleep"] = overlap_cycles(ctx, a, g, g_src, stream, world, make_sleep(a.overlap_compute_ms), nx,
+                                              t_ag)
+        if a.overlap_compute in ("gemm", "both"):
+            overlap["gemm"] = overlap_cycles(ctx, a, g, g_src, stream, world,
+                                             make_compute_small(a.overlap_compute_ms, dev), nx, t_ag)
 
     # ---- e2e through the C ABI with host buffers (daso_step_host) -------------------------------
     e2e = None

@@ -63,6 +63,8 @@ struct daso_ctx {
     unsigned long long* xs = nullptr;
     unsigned long long exch_epoch = 0;            // exchanges this rank has issued
     std::vector<void*> ipc_group;                 // opened group mappings
+    std::vector<cudaStream_t> ce_streams;         // one per other member: the pushes run on parallel copy engines
+    std::vector<cudaEvent_t> ce_done;             // [P-1] fork/join events
 
     // fused mode: node peers' buffers mapped through CUDA IPC (NVLink peer memory)
     float* peer_x[daso::kMaxPeers] = {};
@@ -263,24 +265,26 @@ daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
     }
     CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
-    if (c->ce) {   // copy-engine pushes into every group member's slot (no SMs)
+    if (c->ce) {   // copy-engine pushes into every group member's slot (no SMs), one stream per member
         const unsigned long long e = ++c->exch_epoch;
         const size_t row = size_t(c->seg) * c->wire_bytes;
         Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(row));
-        for (int k = 1; k < c->P && c->exch_enabled; ++k) {
+        for (int k = 1; k < c->P; ++k) {
             const int i = (c->node + k) % c->P;             // start with the next member: spread the links
-            // member i has consumed exchange e-1, so row `node` of its slot is free
-            if (wait_value64()(c->side, CUdeviceptr(c->xs + c->P + i), e - 1, wait_flags(c->device)) != CUDA_SUCCESS)
-                return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange flow control) failed");
-            CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row, own_segment(c),
-                                        row, cudaMemcpyDeviceToDevice, c->side));
-            if (write_value64()(c->side, CUdeviceptr(c->peer_xs[i] + c->node), e, 0) != CUDA_SUCCESS)
+            cudaStream_t cs = c->ce_streams[size_t(k - 1)];
+            CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_packed, 0));
+            if (c->exch_enabled) {
+                // member i has consumed exchange e-1, so row `node` of its slot is free
+                if (wait_value64()(cs, CUdeviceptr(c->xs + c->P + i), e - 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                    return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange flow control) failed");
+                CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row,
+                                            own_segment(c), row, cudaMemcpyDeviceToDevice, cs));
+            }   // else timing knob: flags only, no data
+            if (write_value64()(cs, CUdeviceptr(c->peer_xs[i] + c->node), e, 0) != CUDA_SUCCESS)
                 return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange flag) failed");
+            CUDA_TRY(c, cudaEventRecord(c->ce_done[size_t(k - 1)], cs));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ce_done[size_t(k - 1)], 0));   // join
         }
-        if (!c->exch_enabled)   // timing knob: flags only, no data
-            for (int i = 0; i < c->P; ++i)
-                if (i != c->node && write_value64()(c->side, CUdeviceptr(c->peer_xs[i] + c->node), e, 0) != CUDA_SUCCESS)
-                    return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange flag) failed");
     } else if (c->exch_enabled) {
         Span sp(c, c->side, PH_EXCH, double(c->P - 1) * double(c->seg) * double(c->wire_bytes));
         NCCL_TRY(c, ncclAllGather(own_segment(c), c->slot, size_t(c->seg), wire_nccl(c->cfg.wire), c->group_comm,
@@ -294,11 +298,13 @@ daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
     if (c->vc) return DASO_OK;   // virtual cluster: the loopback copies precede on the same stream
     Span sp(c, s, PH_WAIT, 0.0);
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));   // own outgoing copies / all-gather done
-    if (c->ce)   // every other member's row of this exchange has landed in the slot
-        for (int i = 0; i < c->P; ++i)
-            if (i != c->node &&
-                wait_value64()(s, CUdeviceptr(c->xs + i), c->exch_epoch, wait_flags(c->device)) != CUDA_SUCCESS)
+    if (c->ce)   // every other member's row of this exchange has landed in the slot (flush once, at the last)
+        for (int k = 1; k < c->P; ++k) {
+            const int i = (c->node + k) % c->P;
+            const unsigned flags = k == c->P - 1 ? wait_flags(c->device) : unsigned(CU_STREAM_WAIT_VALUE_GEQ);
+            if (wait_value64()(s, CUdeviceptr(c->xs + i), c->exch_epoch, flags) != CUDA_SUCCESS)
                 return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange arrival) failed");
+        }
     return DASO_OK;
 }
 
@@ -663,6 +669,16 @@ daso_status setup_group_ce(daso_ctx* c) {
         c->ipc_group.push_back(mx);
         c->peer_slot[i] = ms;
         c->peer_xs[i] = static_cast<unsigned long long*>(mx);
+    }
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int k = 1; k < c->P; ++k) {
+        cudaStream_t st = nullptr;
+        cudaEvent_t ev = nullptr;
+        CUDA_TRY(c, cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+        c->ce_streams.push_back(st);
+        CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->ce_done.push_back(ev);
     }
     c->ce = true;
     return DASO_OK;
@@ -1041,10 +1057,15 @@ daso_status daso_exchange_alone(daso_ctx* c, int iters, double* ms_out) {
                                       c->side));
             return DASO_OK;
         }
-        for (int k = 1; k < c->P; ++k) {   // the copy-engine pushes of one exchange, no flags
+        CUDA_TRY(c, cudaEventRecord(c->ev_packed, c->side));
+        for (int k = 1; k < c->P; ++k) {   // the copy-engine pushes of one exchange (parallel streams), no flags
             const int i = (c->node + k) % c->P;
+            cudaStream_t cs = c->ce_streams[size_t(k - 1)];
+            CUDA_TRY(c, cudaStreamWaitEvent(cs, c->ev_packed, 0));
             CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row, own_segment(c),
-                                        row, cudaMemcpyDeviceToDevice, c->side));
+                                        row, cudaMemcpyDeviceToDevice, cs));
+            CUDA_TRY(c, cudaEventRecord(c->ce_done[size_t(k - 1)], cs));
+            CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ce_done[size_t(k - 1)], 0));
         }
         return DASO_OK;
     };
@@ -1079,6 +1100,11 @@ daso_status daso_finalize(daso_ctx* c) {
         for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
         if (c->sig) cudaFree(c->sig);
     }
+    for (cudaStream_t st : c->ce_streams) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    for (cudaEvent_t ev : c->ce_done) cudaEventDestroy(ev);
     if (!c->ipc_group.empty() || c->xs) {
         // no group member may still push into this rank's slot: group barrier before unmapping
         if (c->group_comm && c->xs && c->side) {
