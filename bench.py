@@ -61,8 +61,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--nccl-max-ctas", type=int, default=0, help="cap the side-stream exchange's NCCL CTAs")
-    ap.add_argument("--exchange", choices=["nccl", "ce"], default="nccl",
-                    help="global-tier transport: NCCL all-gather or copy-engine pushes (DASO_EXCH_CE)")
+    ap.add_argument("--exchange", choices=["nccl", "ce"], default="ce",
+                    help="global-tier transport: copy-engine pushes (DASO_EXCH_CE, default: no SMs, hidden behind "
+                         "compute under SM contention) or NCCL all-gather (DASO_EXCH_NCCL)")
     ap.add_argument("--compute-ms", type=float, default=0.0,
                     help="untimed synthetic fwd/bwd stand-in (bf16 GEMMs) between steps, to measure how much of "
                          "the global exchange the next batch's compute hides")
