@@ -380,7 +380,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
     uint64_t* ofull = full + NS;
     uint64_t* oempty = ofull + kWsOut;
     const int tid = threadIdx.x;
-    if (!start_barrier(pa, G)) return;   // 1. start barrier (timed out: error bit raised, do nothing)
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         for (int o = 0; o < kWsOut; ++o) {
@@ -390,24 +389,26 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async_global();
     }
+    if (blockIdx.x == 0 && tid < G) {   // 1a. start barrier, signal half: "my g is ready" to every peer
+        __threadfence_system();
+        st_release_sys(pa.sig_peer[tid] + pa.me, pa.epoch);
+    }
     __syncthreads();
     const int64_t ntiles = a.n / kPT;
     const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     auto tile0 = [&](int64_t k) { return (int64_t(blockIdx.x) + k * gridDim.x) * kPT; };
     bool bad = false;
     if (tid == kWsCompute) {   // ---- the TMA driver
-        auto issue_load = [&](int64_t k) {
+        // Only the peers' gradient tiles need the start barrier: the local part of a stage (own x, v,
+        // own g, slot rows) is issued first, so the first stages load while the signals travel.
+        auto issue_local = [&](int64_t k) {
             const int s = int(k % NS);
             unsigned char* st = smem + size_t(s) * L.in_bytes;
             const int64_t e0 = tile0(k);
             uint32_t tx = (2u + G) * kPT * 4u;
             if constexpr ((OPS & OP_MERGE) != 0) tx += uint32_t(a.P) * kPT * wb;
             mbar_expect_tx(&full[s], tx);
-#pragma unroll
-            for (int q = 0; q < G; ++q) {                       // start with the next peer: spread links
-                const int qq = (pa.me + 1 + q) % G;
-                bulk_g2s(st + L.g + uint32_t(qq) * kPT * 4, pa.gp[qq] + e0, kPT * 4, &full[s]);
-            }
+            bulk_g2s(st + L.g + uint32_t(pa.me) * kPT * 4, pa.gp[pa.me] + e0, kPT * 4, &full[s]);
             bulk_g2s(st + L.x, a.x + e0, kPT * 4, &full[s]);
             bulk_g2s(st + L.v, a.v + e0, kPT * 4, &full[s]);
             if constexpr ((OPS & OP_MERGE) != 0) {
@@ -417,8 +418,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
                              &full[s]);
             }
         };
-        for (int64_t k = 0; k < my && k < NS; ++k) issue_load(k);
-        for (int64_t k = 0; k < my; ++k) {
+        auto issue_remote = [&](int64_t k) {
+            const int s = int(k % NS);
+            unsigned char* st = smem + size_t(s) * L.in_bytes;
+            const int64_t e0 = tile0(k);
+#pragma unroll
+            for (int q = 1; q < G; ++q) {                       // start with the next peer: spread links
+                const int qq = (pa.me + q) % G;
+                bulk_g2s(st + L.g + uint32_t(qq) * kPT * 4, pa.gp[qq] + e0, kPT * 4, &full[s]);
+            }
+        };
+        auto issue_load = [&](int64_t k) {
+            issue_local(k);
+            issue_remote(k);
+        };
+        for (int64_t k = 0; k < my && k < NS; ++k) issue_local(k);
+        bool ok = true;   // 1b. start barrier, wait half: every peer's g is ready
+        for (int q = 0; q < G && ok; ++q) ok = wait_geq(pa.sig_me + q, pa.epoch, pa.err, pa.timeout_ns);
+        // (timed out: error bit raised; the remote tiles are never requested, the compute warps' stage
+        // waits time out as well, and nothing touches peer memory)
+        if (ok)
+            for (int64_t k = 0; k < my && k < NS; ++k) issue_remote(k);
+        for (int64_t k = 0; k < my && ok; ++k) {
             const int o = int(k % kWsOut);
             if (!mbar_wait(&ofull[o], uint32_t((k / kWsOut) & 1), pa.err)) break;
             if (k + NS < my) issue_load(k + NS);                // stage k % NS consumed: refill it
@@ -486,8 +507,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive(&ofull[o]);
         }
-        if (blockIdx.x == gridDim.x - 1)                         // ragged tail through the register path
-            for (int64_t e = ntiles * kPT + tid; e < a.n; e += kWsCompute) peer_body<OPS, WIRE, G, 1>(pa, e, bad);
+        if (blockIdx.x == gridDim.x - 1) {                       // ragged tail through the register path
+            __shared__ int s_tail_ok;                            // it reads peer g: wait for the start barrier
+            if (tid == 0) {
+                bool ok = true;
+                for (int q = 0; q < G && ok; ++q) ok = wait_geq(pa.sig_me + q, pa.epoch, pa.err, pa.timeout_ns);
+                s_tail_ok = ok;
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(kWsCompute) : "memory");   // the compute warps only
+            if (s_tail_ok)
+                for (int64_t e = ntiles * kPT + tid; e < a.n; e += kWsCompute) peer_body<OPS, WIRE, G, 1>(pa, e, bad);
+        }
         if (a.flag != nullptr) {
             const unsigned any = __ballot_sync(0xffffffffu, bad);
             if (any != 0u && (tid & 31) == 0) atomicOr(a.flag, 1u);
