@@ -112,6 +112,7 @@ def main():
     ap.add_argument("--gpus-per-node", type=int, default=0,
                     help="DASO G (default: 2 if world >= 4 else 1); also the node group of SyncBN")
     ap.add_argument("--mode", default="faithful")
+    ap.add_argument("--exchange", choices=["nccl", "ce"], default="nccl", help="global-tier transport")
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--overlap", action="store_true",
                     help="faithful mode: node all-reduce in buckets overlapped with backward (N2)")
@@ -183,10 +184,11 @@ def main():
         uid = daso.rendezvous_unique_id() if world > 1 else daso.daso_get_unique_id()
         if a.train_epochs:
             ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
-                                 total_epochs=max(a.train_epochs, 2), steps_per_epoch=a.steps_per_epoch, mode=a.mode)
+                                 total_epochs=max(a.train_epochs, 2), steps_per_epoch=a.steps_per_epoch, mode=a.mode,
+                                 exchange=a.exchange)
         else:
             ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
-                                 total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode)
+                                 total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode, exchange=a.exchange)
         flat = daso.FlatParams(model.parameters(), gpus_per_node=G)
         ctx.bind(flat.x, flat.g, flat.v, flat.n)
         overlap = daso.OverlappedLocalSync(ctx, flat) if a.overlap else None
@@ -242,7 +244,8 @@ def main():
     if ctx is not None:
         tr = ctx.trace_read(reset=True)
         sync_ms = (tr["kernel_ms"] + tr["local_ms"] + tr["node_ms"] + tr["wait_ms"]) / a.steps
-        out.update({"topology": f"{ctx.P}x{ctx.G}", "mode": a.mode, "overlap": a.overlap, "sync_path_ms_per_step": sync_ms,
+        out.update({"topology": f"{ctx.P}x{ctx.G}", "mode": a.mode, "exchange": a.exchange, "overlap": a.overlap,
+                    "sync_path_ms_per_step": sync_ms,
                     "sync_share": sync_ms / (ms / a.steps), "finite": ctx.check_finite()})
         ctx.finalize()
     if rank == 0:
