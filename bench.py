@@ -452,11 +452,14 @@ def run_ours(a):
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     kind_of = []
+    slack = make_sleep(0.2)         # untimed device work queued before every step: the host always runs
+                                    # ahead, so host-side jitter never leaves the GPU idle inside a window
     with ClockSampler(local) as clk:
         for k in range(a.steps):
             g.copy_(g_src)
             compute()
             l2_flush.sum()          # read-only L2 flush: the step starts cold with a clean L2
+            slack()
             ev0[k].record(stream)
             r = ctx.step(a.lr)
             ev1[k].record(stream)
@@ -494,6 +497,8 @@ def run_ours(a):
         ms_launch = tr["kernel_ms"] / max(tr["kernel_launches"], 1)
         if ms_launch > 0:
             roofline["frac_in_kernel_dram"] = traffic / (ms_launch * 1e-3) / 1e9 / peak
+    plain = [t for t, kk in zip(step_ms, kind_of) if kk == "plain"]
+    p50_plain = max_over_ranks(statistics.median(plain), world) if plain else None
     if a.mode == "fused" and G > 1:
         # the fused node-tier kernel is NVLink-bound: per direction per GPU, (G-1)/G * 4n bytes of
         # gradient shards (peer reads) plus (G-1)/G * 4n bytes of parameter shards (peer stores)
@@ -507,6 +512,7 @@ def run_ours(a):
                     "bytes_per_launch": nvl_bytes, "bytes_def": "NVLink bytes per direction per GPU",
                     "ms_per_launch": tr["kernel_ms"] / max(tr["kernel_launches"], 1),
                     "peak_source": "measured peer copy 770 GB/s per direction (B200_PROFILING.md)",
+                    "frac_at_p50_plain_step": (nvl_bytes / (p50_plain * 1e-3) / 1e9 / 770.0) if p50_plain else None,
                     "probe_ceiling_gbs": 660.0,
                     "frac_of_probe_ceiling": nvl_gbs / 660.0,
                     "probe": "tools/nvlink_kernels.cu tma_rw: this kernel's NVLink traffic pattern with no arithmetic, "
