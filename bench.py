@@ -596,6 +596,7 @@ def run_ours(a):
                                        "overlaps the untimed refresh/flush between steps -- the full-cycle "
                                        "timing with the exchange inside the window is `overlap`",
                        "compute_ms_between_steps": a.compute_ms},
+            "hidden_fraction": ({k: v["hidden_fraction"] for k, v in overlap.items()} if overlap else None),
             "step_kinds": kinds_max, "overlap": overlap, "kernels": kernels,
             "steps_dump": ({"ms": step_ms, "kind": kind_of} if a.dump_steps else None),
             "roofline": roofline, "phases": phases, "gpu_launches": launches_total,
