@@ -270,6 +270,16 @@ def test_copy_engine_exchange(tmp_path, P, G, mode, wire):
     check(ranks, P, G, 4, 1, steps=40, warm=1, cool=1, epochs=5, spe=8, flags="01100", wire=wire)
 
 
+@pytest.mark.parametrize("mode", ["faithful", "fused"])
+def test_copy_engine_exchange_S_equals_B(tmp_path, mode):
+    """DASO_EXCH_CE with S = B = 2 at 2x2: every cycle's first batch merges the previous exchange
+    and starts the next one (R8), so the flow-control acks are on the critical path every cycle;
+    faithful mode adds R11 (the merging group differs from the sending group)."""
+    ranks = run_world(str(tmp_path), 4, ["--P", "2", "--G", "2", "--B", "2", "--S", "2", "--wire", "fp32",
+                                         "--mode", mode, "--exchange", "ce"])
+    check(ranks, 2, 2, 2, 2, wire="fp32")
+
+
 def test_config5_schedule_through_daso_step(tmp_path):
     """Config 5: 1000 batches = 50 epochs x 20, warm-up 5, cool-down 5, B0 = 4,
     S0 = 1, plateau flags Bernoulli(0.3) (seed 7): every record daso_step returns on every rank
