@@ -76,6 +76,7 @@ def parse():
                          "a deterministic device sleep (precise), or both")
     ap.add_argument("--dump-steps", action="store_true", help="add every timed step's ms and kind to the line")
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline table (N=1)")
+    ap.add_argument("--no-vcluster", action="store_true", help="skip the one-GPU 2x4 virtual-cluster block (N=1)")
     ap.add_argument("--ref-div", type=int, default=4,
                     help="reference arm: oracle sample = n / ref-div parameters per step (scaled per parameter)")
     return ap.parse_args()
@@ -309,6 +310,50 @@ def kernel_table(n: int, peak: float, iters: int = 30, warmup: int = 5) -> dict:
         rows[name] = {"bytes_per_param": bpp, "bytes_per_launch": bpp * n, "us_mean": mean, "us_p10": us[len(us) // 10],
                       "us_p90": us[(9 * len(us)) // 10], "achieved_gbs": gbs, "frac": gbs / peak}
     return rows
+
+
+def vcluster_block(n: int, B: int, S: int, peak: float, steps: int = 16, warm: int = 8) -> dict:
+    """The headline 2x4 batch on ONE GPU: a virtual cluster (daso_vcluster_*) runs all 8 ranks' product
+    batches — the fused node-tier kernel (G = 4), bf16 pack, loopback group all-gather, Eq. (1) merge —
+    with every peer buffer in this GPU's HBM.  Each launch's algorithmic bytes (per shard element
+    12 + 8G (+ P*wb merge) (+ wb pack)) all hit local HBM here, so the node-tier kernel
+    gets an HBM roofline; the NVLink roofline needs real GPUs (the N > 1 lines)."""
+    import torch
+    import paper_2104_05588_b200 as daso
+    vc = daso.VCluster(8, 4, B, S, n, total_epochs=1, steps_per_epoch=B * (1 << 20), mode="fused")
+    try:
+        gen = torch.Generator(device="cuda").manual_seed(0)
+        x0 = torch.randn(n, device="cuda", generator=gen) * 0.02
+        for r in range(8):
+            vc.x(r)[:n] = x0
+            vc.g(r)[:n] = torch.randn(n, device="cuda", generator=gen) * 0.01
+        for _ in range(warm):
+            vc.step(0.01)
+        torch.cuda.synchronize()
+        for r in range(8):
+            vc.rank(r).trace_read(reset=True)
+            vc.rank(r).trace_enable(True)
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            vc.step(0.01)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tr = [vc.rank(r).trace_read(reset=True) for r in range(8)]
+        ok = all(vc.rank(r).check_finite() for r in range(8))
+    finally:
+        vc.destroy()
+    k = sum(t["kernel_launches"] for t in tr)
+    ms = sum(t["kernel_ms"] for t in tr)
+    by = sum(t["kernel_bytes"] for t in tr)
+    gbs = by / (ms * 1e-3) / 1e9 if ms else None
+    return {"topology": "2x4 (8 virtual ranks on one GPU)", "B": B, "S": S, "steps": steps,
+            "ms_per_cluster_batch": e0.elapsed_time(e1) / steps, "kernel_launches": k,
+            "us_per_launch": ms / max(k, 1) * 1e3, "bytes_per_launch": by / max(k, 1),
+            "achieved_gbs": gbs, "frac_of_hbm": gbs / peak if gbs else None, "finite": ok,
+            "note": "timing includes the 8 ranks' batches run one after another plus the loopback copies; "
+                    "the per-launch figures are the library's CUDA-event spans of its kernels"}
 
 
 def pct(xs, q):
@@ -572,9 +617,14 @@ def run_ours(a):
     ctx.finalize()
 
     kernels = None
+    vcb = None
     if world == 1 and not a.no_kernels:
         with ClockSampler(local) as kclk:
             kernels = kernel_table(n, peak)
+        if not a.no_vcluster:
+            with ClockSampler(local) as vclk:
+                vcb = vcluster_block(n, a.B, a.S, peak)
+            vcb["clocks"] = vclk.summary()
         kernels = {"n_params": n, "peak_gbs": peak, "peak_source": peak_src, "clocks": kclk.summary(),
                    "timing": "CUDA events on the launching stream around each launch, 256 MB L2 flush between "
                              "launches, 30 launches after 5 warm-up; achieved = algorithmic bytes / mean time",
@@ -597,7 +647,7 @@ def run_ours(a):
                                        "timing with the exchange inside the window is `overlap`",
                        "compute_ms_between_steps": a.compute_ms},
             "hidden_fraction": ({k: v["hidden_fraction"] for k, v in overlap.items()} if overlap else None),
-            "step_kinds": kinds_max, "overlap": overlap, "kernels": kernels,
+            "step_kinds": kinds_max, "overlap": overlap, "kernels": kernels, "vcluster_2x4": vcb,
             "steps_dump": ({"ms": step_ms, "kind": kind_of} if a.dump_steps else None),
             "roofline": roofline, "phases": phases, "gpu_launches": launches_total,
             "gpu_launches_per_rank": tr["kernel_launches"],
