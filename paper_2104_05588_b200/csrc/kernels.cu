@@ -82,7 +82,8 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
 // Eight parameters per thread for every op set.  Measured alternatives (profiles/r01): 32 per
 // thread for the light kernels (average, pack) was slower (K4 41 -> 57 us, pack 23 -> 37 us); a
 // K4 with P templated and two chunks per thread, all 2P row loads in flight before the sums, ran
-// 42.0 vs 42.4 us at P = 2 and 57.6 vs 53.2 us at P = 4 (profiles/r02/k4_variants.txt), and
+// 42.0 vs 42.4 us at P = 2 and 57.6 vs 53.2 us at P = 4, and a TMA-staged K4 (bulk row loads, bulk x
+// store, persistent CTAs) 97.4 us (profiles/r02/k4_variants.txt); and
 // issuing the two 128-bit loads of a stream from an array loop instead of two named loads cost K1
 // 9 % (75 -> 82 us, same box, A/B in one run): ptxas schedules the explicit form better.
 template <int OPS, int WIRE>
@@ -235,78 +236,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) tma_kernel(const KernelArgs a,
     }
 }
 
-// ----------------------------------------------------------------- TMA-staged K4
-// The blocking average (Fig. 3) with the P slot rows of a 2048-parameter tile brought in by bulk
-// copies (one mbarrier per stage, completion counted in bytes) and the averaged fp32 tile written
-// back by a bulk store; one persistent CTA per SM, NS stages in flight.  Same sum order as
-// body<OP_AVERAGE> (0 + s_0 + s_1 + ..., then / P).  Selected with DASO_K4=tma.
-template <int WIRE>
-__global__ void __launch_bounds__(kTmaThreads, 1) average_tma_kernel(const KernelArgs a, int NS) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
-    const uint32_t rows = uint32_t(a.P) * kTile * wb, stage = (rows + kTile * 4 + 127) / 128 * 128;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + size_t(NS) * stage);
-    const int64_t ntiles = a.n / kTile;
-    const int64_t my = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const bool leader = threadIdx.x == 0;
-    if (leader) {
-        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue_load = [&](int64_t k) {
-        const int s = int(k % NS);
-        unsigned char* st = smem + size_t(s) * stage;
-        const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kTile;
-        mbar_expect_tx(&full[s], rows);
-        for (int p = 0; p < a.P; ++p)
-            bulk_g2s(st + uint32_t(p) * kTile * wb,
-                     static_cast<const unsigned char*>(a.slot) + (p * a.slot_stride + e0) * wb, kTile * wb, &full[s]);
-    };
-    if (leader)
-        for (int64_t k = 0; k < my && k < NS; ++k) issue_load(k);
-    bool bad = false;
-    for (int64_t k = 0; k < my; ++k) {
-        const int s = int(k % NS);
-        unsigned char* st = smem + size_t(s) * stage;
-        if (!mbar_wait(&full[s], uint32_t((k / NS) & 1), a.err)) break;
-        const int i = threadIdx.x * kVec;
-        float x[kVec];
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) x[j] = 0.f;
-        for (int p = 0; p < a.P; ++p) {
-            float sv[kVec];
-            Wire<WIRE>::template load_smem<kVec>(st + uint32_t(p) * kTile * wb, i, sv);
-#pragma unroll
-            for (int j = 0; j < kVec; ++j) x[j] += sv[j];
-        }
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) {
-            x[j] = x[j] / a.den;
-            bad |= !isfinite(x[j]);
-        }
-        Wire<DASO_WIRE_FP32>::template store_smem<kVec>(st + rows, i, x);
-        fence_async_smem();
-        __syncthreads();
-        if (leader) {
-            const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kTile;
-            bulk_s2g(a.x + e0, st + rows, kTile * 4);
-            bulk_commit();
-            if (k >= 1 && k - 1 + NS < my) {   // stage of tile k-1 is free once its store has read it
-                bulk_wait_read<1>();
-                issue_load(k - 1 + NS);
-            }
-        }
-    }
-    if (leader) bulk_wait_all();
-    if (blockIdx.x == gridDim.x - 1)
-        for (int64_t e = ntiles * kTile + threadIdx.x; e < a.n; e += blockDim.x) body<OP_AVERAGE, WIRE, 1>(a, e, bad);
-    if (a.flag != nullptr) {
-        const unsigned any = __ballot_sync(0xffffffffu, bad);
-        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
-    }
-}
-
 // ----------------------------------------------------------------- launch config
 struct DevInfo {
     int sms = 0;
@@ -369,34 +298,6 @@ int launch_tma(const KernelArgs& a, cudaStream_t s) {
     return int(cudaGetLastError());
 }
 
-// K4 data path (DASO_K4=tma|ldg; default ldg until measured otherwise)
-int k4_impl() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("DASO_K4");
-        v = (e && strcmp(e, "tma") == 0) ? 1 : 0;
-    }
-    return v;
-}
-
-template <int WIRE>
-int launch_average_tma(const KernelArgs& a, cudaStream_t s) {
-    constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
-    const uint32_t rows = uint32_t(a.P) * kTile * wb, stage = (rows + kTile * 4 + 127) / 128 * 128;
-    const int NS = int(std::min<int64_t>(8, (200 * 1024) / stage));
-    if (NS < 2) return launch_t<OP_AVERAGE, WIRE>(a, s);
-    const size_t smem = size_t(NS) * stage + 8 * size_t(NS);
-    static size_t attr = 0;
-    if (smem > attr) {
-        const cudaError_t e = cudaFuncSetAttribute(average_tma_kernel<WIRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   int(smem));
-        if (e != cudaSuccess) return int(e);
-        attr = smem;
-    }
-    average_tma_kernel<WIRE><<<dim3(unsigned(sm_count())), dim3(kTmaThreads), smem, s>>>(a, NS);
-    return int(cudaGetLastError());
-}
-
 bool tma_ok(const KernelArgs& a, int wb) {
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
     return a.n >= kTile && al(a.x) && al(a.v) && al(a.g) && (a.pack_out == nullptr || al(a.pack_out)) &&
@@ -422,11 +323,7 @@ int dispatch(int ops, const KernelArgs& a, cudaStream_t s) {
         case OP_UPDATE | OP_MERGE | OP_PACK: return launch_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(a, s);
         case OP_MERGE: return launch_t<OP_MERGE, WIRE>(a, s);
         case OP_MERGE | OP_PACK: return launch_t<OP_MERGE | OP_PACK, WIRE>(a, s);
-        case OP_AVERAGE:
-            if (k4_impl() == 1 && a.n >= kTile && (reinterpret_cast<uintptr_t>(a.x) & 15u) == 0 &&
-                (reinterpret_cast<uintptr_t>(a.slot) & 15u) == 0 && (a.slot_stride * wb) % 16 == 0)
-                return launch_average_tma<WIRE>(a, s);
-            return launch_t<OP_AVERAGE, WIRE>(a, s);
+        case OP_AVERAGE: return launch_t<OP_AVERAGE, WIRE>(a, s);
         case OP_PACK: return launch_t<OP_PACK, WIRE>(a, s);
         default: return int(cudaErrorInvalidValue);
     }

@@ -148,41 +148,6 @@ def test_k4_average(n, P):
     close(X.cpu().numpy(), numerics.average([rows[i, :n] for i in range(P)]))
 
 
-_K4_CHILD = """
-import sys, numpy as np, torch
-sys.path.insert(0, sys.argv[1])
-import paper_2104_05588_b200 as daso
-out = {}
-for n, P in ((4099, 2), (3 * 2 ** 16 + 5, 2), (3 * 2 ** 16 + 5, 3), (2048 * 300 + 17, 8)):
-    stride = (n + 63) // 64 * 64
-    g = torch.Generator(device="cuda").manual_seed(n + P)
-    slot = (torch.randn(P, stride, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    x = torch.zeros(n, device="cuda")
-    daso.daso_k_average(x, slot, wire="bf16")
-    out[f"{n}_{P}"] = x.cpu().numpy()
-np.savez(sys.argv[2], **out)
-"""
-
-
-@pytest.mark.parametrize("wire", ["bf16"])
-def test_k4_tma_path_bit_identical(tmp_path, wire):
-    """The TMA-staged blocking average (DASO_K4=tma: bulk copies of the P slot rows, bulk store of x)
-    computes bitwise what the register-path K4 computes (same sum order), multi-tile + ragged sizes."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for impl in ("ldg", "tma"):
-        f = str(tmp_path / f"{impl}.npz")
-        r = subprocess.run([sys.executable, "-c", _K4_CHILD, root, f], env={**os.environ, "DASO_K4": impl},
-                           capture_output=True, text=True, timeout=300)
-        assert r.returncode == 0, r.stderr[-3000:]
-        res[impl] = np.load(f)
-    for k in res["ldg"].files:
-        np.testing.assert_array_equal(res["ldg"][k].view(np.uint32), res["tma"][k].view(np.uint32))
-
-
 @pytest.mark.parametrize("n", [1, 9, 4099])
 def test_merge_only_and_pack_only(n):
     stride = (n + 63) // 64 * 64
