@@ -312,7 +312,7 @@ def kernel_table(n: int, peak: float, iters: int = 30, warmup: int = 5) -> dict:
     return rows
 
 
-def vcluster_block(n: int, B: int, S: int, peak: float, steps: int = 16, warm: int = 8) -> dict:
+def vcluster_block(n: int, B: int, S: int, peak: float, exchange: str, steps: int = 16, warm: int = 8) -> dict:
     """The headline 2x4 batch on ONE GPU: a virtual cluster (daso_vcluster_*) runs all 8 ranks' product
     batches — the fused node-tier kernel (G = 4), bf16 pack, loopback group all-gather, Eq. (1) merge —
     with every peer buffer in this GPU's HBM.  Each launch's algorithmic bytes (per shard element
@@ -320,7 +320,8 @@ def vcluster_block(n: int, B: int, S: int, peak: float, steps: int = 16, warm: i
     gets an HBM roofline; the NVLink roofline needs real GPUs (the N > 1 lines)."""
     import torch
     import paper_2104_05588_b200 as daso
-    vc = daso.VCluster(8, 4, B, S, n, total_epochs=1, steps_per_epoch=B * (1 << 20), mode="fused")
+    vc = daso.VCluster(8, 4, B, S, n, total_epochs=1, steps_per_epoch=B * (1 << 20), mode="fused",
+                       exchange=exchange)
     try:
         gen = torch.Generator(device="cuda").manual_seed(0)
         x0 = torch.randn(n, device="cuda", generator=gen) * 0.02
@@ -348,7 +349,7 @@ def vcluster_block(n: int, B: int, S: int, peak: float, steps: int = 16, warm: i
     ms = sum(t["kernel_ms"] for t in tr)
     by = sum(t["kernel_bytes"] for t in tr)
     gbs = by / (ms * 1e-3) / 1e9 if ms else None
-    return {"topology": "2x4 (8 virtual ranks on one GPU)", "B": B, "S": S, "steps": steps,
+    return {"topology": "2x4 (8 virtual ranks on one GPU)", "B": B, "S": S, "exchange": exchange, "steps": steps,
             "ms_per_cluster_batch": e0.elapsed_time(e1) / steps, "kernel_launches": k,
             "us_per_launch": ms / max(k, 1) * 1e3, "bytes_per_launch": by / max(k, 1),
             "achieved_gbs": gbs, "frac_of_hbm": gbs / peak if gbs else None, "finite": ok,
@@ -623,7 +624,7 @@ def run_ours(a):
             kernels = kernel_table(n, peak)
         if not a.no_vcluster:
             with ClockSampler(local) as vclk:
-                vcb = vcluster_block(n, a.B, a.S, peak)
+                vcb = vcluster_block(n, a.B, a.S, peak, a.exchange)
             vcb["clocks"] = vclk.summary()
         kernels = {"n_params": n, "peak_gbs": peak, "peak_source": peak_src, "clocks": kclk.summary(),
                    "timing": "CUDA events on the launching stream around each launch, 256 MB L2 flush between "

@@ -259,7 +259,7 @@ int wait_flags(int device) {   // GEQ, plus a flush of remote writes where the d
 // Non-blocking global exchange: after the packing kernel on the compute
 // stream, the side stream runs the in-place group all-gather of the slot.
 daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
-    if (c->vc) {   // virtual cluster: the driver copies every packed row after all ranks ran
+    if (c->vc && !c->ce) {   // virtual cluster, loopback: the driver copies every packed row after all ranks ran
         c->vc_sent = true;
         return DASO_OK;
     }
@@ -295,7 +295,7 @@ daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
 }
 
 daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
-    if (c->vc) return DASO_OK;   // virtual cluster: the loopback copies precede on the same stream
+    if (c->vc && !c->ce) return DASO_OK;   // virtual cluster, loopback: the copies precede on the same stream
     Span sp(c, s, PH_WAIT, 0.0);
     CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_exchanged, 0));   // own outgoing copies / all-gather done
     if (c->ce)   // every other member's row of this exchange has landed in the slot (flush once, at the last)
@@ -311,7 +311,7 @@ daso_status wait_exchange(daso_ctx* c, cudaStream_t s) {
 // The slot rows of the current exchange have been read (merge / blocking average issued on s):
 // tell every member its row in this rank's slot may be overwritten (copy-engine exchange only).
 daso_status exchange_consumed(daso_ctx* c, cudaStream_t s) {
-    if (!c->ce || c->vc) return DASO_OK;
+    if (!c->ce) return DASO_OK;
     for (int i = 0; i < c->P; ++i)
         if (i != c->node && write_value64()(s, CUdeviceptr(c->peer_xs[i] + c->P + c->node), c->exch_epoch, 0) != CUDA_SUCCESS)
             return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange ack) failed");
@@ -1212,6 +1212,35 @@ daso_status daso_vcluster_create(daso_vcluster** out, int world, int gpus_per_no
             }
         }
     }
+    if (cfg->exchange == DASO_EXCH_CE && v->P > 1) {
+        // the real copy-engine exchange between sibling ranks on this GPU: same-device copies and the same
+        // stream memory-op flags / acks as across GPUs (no kernel waits on another: the waits are stream waits)
+        if (!write_value64() || !wait_value64()) return v->fail(DASO_ERR_CONFIG, "stream memory operations unavailable");
+        const size_t xs_bytes = (2 * size_t(v->P) + 1) * sizeof(unsigned long long);
+        for (daso_ctx* c : v->rank) {
+            if (cudaMalloc(&c->xs, xs_bytes) != cudaSuccess || cudaMemset(c->xs, 0, xs_bytes) != cudaSuccess)
+                return v->fail(DASO_ERR_CUDA, "virtual cluster: flag allocation failed");
+        }
+        for (daso_ctx* c : v->rank) {
+            c->peer_slot.assign(size_t(v->P), nullptr);
+            c->peer_xs.assign(size_t(v->P), nullptr);
+            for (int i = 0; i < v->P; ++i) {
+                daso_ctx* m = v->rank[size_t(i) * v->G + c->local];   // group member on node i
+                c->peer_slot[i] = m->slot;
+                c->peer_xs[i] = m->xs;
+            }
+            for (int k = 1; k < v->P; ++k) {
+                cudaStream_t st = nullptr;
+                cudaEvent_t ev = nullptr;
+                if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+                    return v->fail(DASO_ERR_CUDA, "virtual cluster: stream creation failed");
+                c->ce_streams.push_back(st);
+                c->ce_done.push_back(ev);
+            }
+            c->ce = true;
+        }
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) return v->fail(DASO_ERR_CUDA, "virtual cluster: setup failed");
     return DASO_OK;
 }
@@ -1247,7 +1276,7 @@ daso_status daso_vcluster_step(daso_vcluster* v, float lr, int plateau, void* st
         sent |= c->vc_sent;
         blocking |= c->vc_blocking;
     }
-    if (sent) {   // loopback group all-gather: member (i, l)'s packed row -> row i of every member (j, l)
+    if (sent && !v->rank[0]->ce) {   // loopback group all-gather: member (i, l)'s packed row -> row i of every member (j, l)
         const size_t wb = v->rank[0]->wire_bytes, seg = size_t(v->rank[0]->seg);
         for (int l = 0; l < v->G; ++l)
             for (int i = 0; i < v->P; ++i) {

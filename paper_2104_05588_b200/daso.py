@@ -265,10 +265,12 @@ class VCluster:
     def __init__(self, world: int, gpus_per_node: int, B: int, S: int, n: int, *, warmup_epochs: int = 0,
                  cooldown_epochs: int = 0, total_epochs: int = 1, steps_per_epoch: int = 1 << 20,
                  momentum: float = 0.9, weight_decay: float = 1e-4, wire: str = "bf16", mode: str = "fused",
-                 check_finite: bool = True):
+                 check_finite: bool = True, exchange: str = "nccl"):
+        """exchange="nccl": the group all-gather is emulated by loopback copies; "ce": the real
+        copy-engine exchange (DASO_EXCH_CE) runs between the sibling ranks on this GPU."""
         torch = _torch()
         cfg = _config(0, warmup_epochs, cooldown_epochs, total_epochs, steps_per_epoch, momentum, weight_decay,
-                      wire, mode, check_finite, 0)
+                      wire, mode, check_finite, 0, exchange)
         h = C.c_void_p()
         s = lib().daso_vcluster_create(C.byref(h), world, gpus_per_node, B, S, C.byref(cfg), int(n))
         if s != L.OK:

@@ -22,13 +22,13 @@ from parity_util import check_trajectory, toy_oracle  # noqa: E402
 
 
 def run_vc(P, G, B, S, steps=20, d=1000, b=32, lr=0.01, mu=0.9, wd=1e-4, wire="bf16", warm=0, cool=0, epochs=1,
-           spe=20, flags="", mode="fused", kernel=None, keep_trace=True):
+           spe=20, flags="", mode="fused", kernel=None, keep_trace=True, exchange="nccl"):
     torch.cuda.set_device(0)
     torch.backends.cuda.matmul.allow_tf32 = False
     prev = daso.daso_kernel_impl(kernel) if kernel else None
     W = P * G
     vc = daso.VCluster(W, G, B, S, d, warmup_epochs=warm, cooldown_epochs=cool, total_epochs=epochs,
-                       steps_per_epoch=spe, momentum=mu, weight_decay=wd, wire=wire, mode=mode)
+                       steps_per_epoch=spe, momentum=mu, weight_decay=wd, wire=wire, mode=mode, exchange=exchange)
     try:
         fl = [int(c) for c in flags]
         traces = [[] for _ in range(W)]
@@ -119,6 +119,22 @@ def test_vcluster_one_gpu_per_node_modes(P, mode):
     kw = dict(steps=40, warm=1, cool=1, epochs=5, spe=8, flags="01100", wire="bf16")
     traces, recs = run_vc(P, 1, 4, 1, mode=mode, **kw)
     check_trajectory(traces, recs, toy_oracle(P, 1, 4, 1, **kw), P, 1, "bf16")
+
+
+@pytest.mark.parametrize("P,G,B,S,mode", [(2, 2, 4, 1, "fused"), (2, 4, 4, 1, "fused"), (4, 2, 4, 1, "fused"),
+                                          (8, 1, 4, 1, "fused"), (2, 2, 2, 2, "fused"), (4, 1, 2, 2, "faithful")])
+@pytest.mark.parametrize("wire", ["bf16", "fp32"])
+def test_vcluster_copy_engine_exchange(P, G, B, S, mode, wire):
+    """The global tier's copy-engine exchange (DASO_EXCH_CE, the bench default) for real, between the
+    sibling ranks on one GPU: same-device cudaMemcpyAsync pushes into the group members' slots, the
+    cuStreamWriteValue64 arrival flags and consumed acks, cuStreamWaitValue64 at the merge — the full
+    schedule (blocking warm-up / cool-down, cycling with plateau halving; S = B puts the flow-control
+    acks on the critical path of every cycle) against the oracle."""
+    spe = 8 if B <= 4 else 16
+    kw = dict(steps=40, warm=1, cool=1, epochs=5, spe=spe, flags="01100", wire=wire, mode=mode)
+    traces, recs = run_vc(P, G, B, S, exchange="ce", **kw)
+    kw.pop("mode")
+    check_trajectory(traces, recs, toy_oracle(P, G, B, S, **kw), P, G, wire)
 
 
 def test_vcluster_config5_schedule_2x4():
