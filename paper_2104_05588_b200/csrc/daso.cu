@@ -256,13 +256,20 @@ int wait_flags(int device) {   // GEQ, plus a flush of remote writes where the d
 }
 
 // ---- collectives ---------------------------------------------------------------
+daso_status push_exchange(daso_ctx* c, cudaStream_t s);
+
 // Non-blocking global exchange: after the packing kernel on the compute
 // stream, the side stream runs the in-place group all-gather of the slot.
 daso_status start_exchange(daso_ctx* c, cudaStream_t s) {
-    if (c->vc && !c->ce) {   // virtual cluster, loopback: the driver copies every packed row after all ranks ran
+    if (c->vc) {   // virtual cluster: the driver issues the exchange after every rank's batch (see there)
         c->vc_sent = true;
         return DASO_OK;
     }
+    return push_exchange(c, s);
+}
+
+// The send itself: after the pack on `s`, the group all-gather (NCCL) or the copy-engine pushes.
+daso_status push_exchange(daso_ctx* c, cudaStream_t s) {
     CUDA_TRY(c, cudaEventRecord(c->ev_packed, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_packed, 0));
     if (c->ce) {   // copy-engine pushes into every group member's slot (no SMs), one stream per member
@@ -1276,7 +1283,18 @@ daso_status daso_vcluster_step(daso_vcluster* v, float lr, int plateau, void* st
         sent |= c->vc_sent;
         blocking |= c->vc_blocking;
     }
-    if (sent && !v->rank[0]->ce) {   // loopback group all-gather: member (i, l)'s packed row -> row i of every member (j, l)
+    if (sent && v->rank[0]->ce) {
+        // the real copy-engine exchange, issued only now: every rank's merge and its consumed acks are
+        // already enqueued, so every stream wait (flow control on the copy streams, arrival at a later
+        // merge) depends only on earlier work — within one process streams share hardware queues, and a
+        // wait on a flag that later work of the same process writes could block that very work
+        for (size_t i = 0; i < v->rank.size(); ++i) {
+            daso_ctx* c = v->rank[i];
+            if (!c->vc_sent) continue;
+            const daso_status st = push_exchange(c, s);
+            if (st != DASO_OK) return v->fail(st, "rank " + std::to_string(i) + ": " + c->err);
+        }
+    } else if (sent) {   // loopback group all-gather: member (i, l)'s packed row -> row i of every member (j, l)
         const size_t wb = v->rank[0]->wire_bytes, seg = size_t(v->rank[0]->seg);
         for (int l = 0; l < v->G; ++l)
             for (int i = 0; i < v->P; ++i) {
