@@ -189,8 +189,12 @@ def main():
         else:
             ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
                                  total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode, exchange=a.exchange)
-        flat = daso.FlatParams(model.parameters(), gpus_per_node=G)
-        ctx.bind(flat.x, flat.g, flat.v, flat.n)
+        if a.mode == "fused" and "expandable_segments:True" in os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""):
+            # cuMem-backed torch memory cannot be exported by CUDA IPC: let the library own the buckets
+            flat = daso.FlatParams(model.parameters(), gpus_per_node=G, ctx=ctx)
+        else:
+            flat = daso.FlatParams(model.parameters(), gpus_per_node=G)
+            ctx.bind(flat.x, flat.g, flat.v, flat.n)
         overlap = daso.OverlappedLocalSync(ctx, flat) if a.overlap else None
         net = model
 
