@@ -244,6 +244,9 @@ typedef struct {
     int64_t node_ops;         double node_ms;    double node_bytes;    /* node broadcast / all-gather of x (bus bytes) */
     int64_t wait_ops;         double wait_ms;                          /* compute-stream time blocked on the exchange */
     int64_t exch_ops;         double exch_ms;    double exch_bytes;    /* side-stream group all-gathers (bytes received) */
+    double kernel_nvl_bytes;  /* NVLink bytes per direction of the fused-mode node-tier launches (counted in
+                                 kernel_*): (G-1) * 4 B per shard element for each of the peer gradient reads
+                                 and the peer parameter stores a launch performs */
 } daso_trace;
 daso_status daso_trace_enable(daso_ctx* c, int on);
 daso_status daso_trace_read(daso_ctx* c, daso_trace* out, int reset);

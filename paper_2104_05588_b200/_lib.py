@@ -50,7 +50,8 @@ TRACE_FIELDS = [("steps", C.c_int64), ("kernel_launches", C.c_int64), ("kernel_m
                 ("kernel_bytes", C.c_double), ("local_ops", C.c_int64), ("local_ms", C.c_double),
                 ("local_bytes", C.c_double), ("node_ops", C.c_int64), ("node_ms", C.c_double),
                 ("node_bytes", C.c_double), ("wait_ops", C.c_int64), ("wait_ms", C.c_double),
-                ("exch_ops", C.c_int64), ("exch_ms", C.c_double), ("exch_bytes", C.c_double)]
+                ("exch_ops", C.c_int64), ("exch_ms", C.c_double), ("exch_bytes", C.c_double),
+                ("kernel_nvl_bytes", C.c_double)]
 
 
 class Trace(C.Structure):

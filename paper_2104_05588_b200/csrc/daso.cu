@@ -89,7 +89,7 @@ struct daso_ctx {
     std::string err;
 
     // tracing (daso_trace_enable / daso_trace_read)
-    struct SpanRec { cudaEvent_t a, b; int phase; double bytes; };
+    struct SpanRec { cudaEvent_t a, b; int phase; double bytes, nvl; };
     bool tracing = false;
     std::vector<cudaEvent_t> pool;
     size_t pool_used = 0;
@@ -191,9 +191,9 @@ struct Span {   // RAII event pair around one phase on one stream
     daso_ctx* c;
     cudaStream_t s;
     int phase;
-    double bytes;
+    double bytes, nvl;
     cudaEvent_t a = nullptr;
-    Span(daso_ctx* c_, cudaStream_t s_, int ph, double b) : c(c_), s(s_), phase(ph), bytes(b) {
+    Span(daso_ctx* c_, cudaStream_t s_, int ph, double b, double nvl_ = 0.0) : c(c_), s(s_), phase(ph), bytes(b), nvl(nvl_) {
         if (c->tracing && (a = next_event(c)) != nullptr) cudaEventRecord(a, s);
     }
     ~Span() {
@@ -201,7 +201,7 @@ struct Span {   // RAII event pair around one phase on one stream
         cudaEvent_t b = next_event(c);
         if (!b) return;
         cudaEventRecord(b, s);
-        c->spans.push_back({a, b, phase, bytes});
+        c->spans.push_back({a, b, phase, bytes, nvl});
     }
 };
 
@@ -356,20 +356,54 @@ daso_status shard_blocking_tail(daso_ctx* c, cudaStream_t s) {   // sharded / fu
     return exchange_consumed(c, s);
 }
 
+// Node-tier kernel arguments common to the fused batch and the fused blocking tail: peer
+// pointer tables at this rank's shard, signal arrays, a fresh barrier epoch.
+daso_status fused_peer_args(daso_ctx* c, daso::PeerArgs& pa, int64_t off, int64_t sh, float lr, cudaStream_t s) {
+    pa.a = base_args(c, off, sh, lr);
+    for (int q = 0; q < c->G; ++q) {
+        pa.xp[q] = c->peer_x[q] + off;
+        pa.gp[q] = c->peer_g[q] + off;
+        pa.sig_peer[q] = c->peer_sig[q];
+    }
+    pa.sig_me = c->sig;
+    pa.done = reinterpret_cast<unsigned*>(c->sig + 2 * c->G);
+    pa.err = c->d_flag;
+    pa.epoch = ++c->epoch;
+    if (c->vc) {
+        // Virtual cluster: the node's G kernels run one after another on one stream, so no
+        // launch may wait for a later one (B200 guide: never launch kernels that wait on each
+        // other on one GPU).  The first rank of the node pre-sets every start and end signal
+        // of the node to this epoch, so every barrier wait is satisfied at its first poll;
+        // the kernels' own signal stores write the same values.  Stream order provides what
+        // the barriers provide across GPUs (all g complete before any read; all x stores
+        // complete before the next batch), and shards are disjoint, so the sequential
+        // execution computes exactly what G concurrent GPUs compute.
+        if (c->local == 0) KERN_TRY(c, daso::launch_fill_u64(c->vc_node_sig, c->G, 2 * c->G + 2, 2 * c->G, pa.epoch, s));
+        pa.timeout_ns = 1000ull * 1000 * 1000;
+    }
+    pa.G = c->G;
+    pa.me = c->local;
+    return DASO_OK;
+}
+
+// Fig. 3 average + Fig. 4 re-publish in one kernel (launch_avg_publish): the averaged shard goes
+// straight into every node peer's x over NVLink, and the kernel's end barrier (which also
+// covers the preceding OP_NOX node-tier kernel's gradient reads) orders it before any rank's
+// next read of x.
 daso_status fused_blocking_tail(daso_ctx* c, cudaStream_t s) {
     const int64_t sh = c->seg, off = int64_t(c->local) * sh;
-    STATUS_TRY(shard_blocking_tail(c, s));
-    // re-publish the averaged shard to the node peers (NVLink copies) ...
-    for (int q = 0; q < c->G; ++q) {
-        if (q == c->local) continue;
-        CUDA_TRY(c, cudaMemcpyAsync(c->peer_x[q] + off, c->x + off, size_t(sh) * 4, cudaMemcpyDeviceToDevice, s));
+    STATUS_TRY(wait_exchange(c, s));
+    daso::PeerArgs pa;
+    STATUS_TRY(fused_peer_args(c, pa, off, sh, 0.f, s));
+    pa.a.den = float(c->P);
+    {
+        // HBM bytes on THIS GPU per shard element: P slot rows read, own x written, and the G-1
+        // peers' stores into this GPU's x (symmetric); NVLink per direction (G-1) * 4.
+        Span sp(c, s, PH_KERNEL, (double(c->P) * double(c->wire_bytes) + 4.0 * c->G) * double(sh),
+                4.0 * (c->G - 1) * double(sh));
+        KERN_TRY(c, daso::launch_avg_publish(c->cfg.wire, pa, s));
     }
-    // ... and the peers must see every shard before their next read of x: node barrier
-    // (a virtual cluster's ranks share one stream, which already orders them)
-    if (!c->vc)
-        NCCL_TRY(c, ncclAllReduce(c->sig + 2 * c->G + 1, c->sig + 2 * c->G + 1, 1, ncclUint64, ncclSum,
-                                  c->node_comm, s));
-    return DASO_OK;
+    return exchange_consumed(c, s);
 }
 
 daso_status finish_blocking(daso_ctx* c, cudaStream_t s) {   // virtual cluster, after the loopback exchange
@@ -494,7 +528,7 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
     const bool merge = global && r.merge;
     const bool send = global && r.send;
     daso::PeerArgs pa;
-    pa.a = base_args(c, off, sh, lr);
+    STATUS_TRY(fused_peer_args(c, pa, off, sh, lr, s));
     int ops = daso::OP_UPDATE;
     if (merge) {
         STATUS_TRY(wait_exchange(c, s));
@@ -505,38 +539,19 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
     if (send) {
         ops |= daso::OP_PACK;
         pa.a.pack_out = own_segment(c);
+        // blocking batch: the average of the tail replaces x, so the node-tier kernel only
+        // packs (no x stores to the peers, no end barrier: the tail's end barrier covers it)
+        if (r.blocking) ops |= daso::OP_NOX;
     }
-    for (int q = 0; q < c->G; ++q) {
-        pa.xp[q] = c->peer_x[q] + off;
-        pa.gp[q] = c->peer_g[q] + off;
-        pa.sig_peer[q] = c->peer_sig[q];
-    }
-    pa.sig_me = c->sig;
-    pa.done = reinterpret_cast<unsigned*>(c->sig + 2 * c->G);
-    pa.err = c->d_flag;
-    pa.epoch = ++c->epoch;
-    if (c->vc) {
-        // Virtual cluster: the node's G kernels run one after another on one stream, so no
-        // launch may wait for a later one (B200 guide: never launch kernels that wait on each
-        // other on one GPU).  The first rank of the node pre-sets every start and end signal
-        // of the node to this epoch, so every barrier wait is satisfied at its first poll;
-        // the kernels' own signal stores write the same values.  Stream order provides what
-        // the barriers provide across GPUs (all g complete before any read; all x stores
-        // complete before the next batch), and shards are disjoint, so the sequential
-        // execution computes exactly what G concurrent GPUs compute.
-        if (c->local == 0) KERN_TRY(c, daso::launch_fill_u64(c->vc_node_sig, c->G, 2 * c->G + 2, 2 * c->G, pa.epoch, s));
-        pa.timeout_ns = 1000ull * 1000 * 1000;
-    }
-    pa.G = c->G;
-    pa.me = c->local;
     {
         // HBM bytes on THIS GPU per shard element: own x r + w, v r + w, own g r
         // (20) + the G-1 peers reading this GPU's g and writing its x (8 (G-1)) + slot rows / pack.
         // NVLink per direction: (G-1) * 4 B per shard element (bench.py reports it separately).
         const double wb = double(c->wire_bytes);
-        double per = 20.0 + 8.0 * (c->G - 1) + ((ops & daso::OP_MERGE) ? c->P * wb : 0) +
-                     ((ops & daso::OP_PACK) ? wb : 0);
-        Span sp(c, s, PH_KERNEL, per * double(sh));
+        double per = ((ops & daso::OP_NOX) ? 16.0 + 4.0 * (c->G - 1) : 20.0 + 8.0 * (c->G - 1)) +
+                     ((ops & daso::OP_MERGE) ? c->P * wb : 0) + ((ops & daso::OP_PACK) ? wb : 0);
+        const double nvl = ((ops & daso::OP_NOX) ? 1.0 : 2.0) * 4.0 * (c->G - 1) * double(sh);
+        Span sp(c, s, PH_KERNEL, per * double(sh), nvl);
         KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
     }
     if (merge) STATUS_TRY(exchange_consumed(c, s));
@@ -994,7 +1009,10 @@ daso_status daso_trace_read(daso_ctx* c, daso_trace* out, int reset) {
         float ms = 0.f;
         CUDA_TRY(c, cudaEventElapsedTime(&ms, sp.a, sp.b));
         switch (sp.phase) {
-            case PH_KERNEL: c->acc.kernel_launches++; c->acc.kernel_ms += ms; c->acc.kernel_bytes += sp.bytes; break;
+            case PH_KERNEL:
+                c->acc.kernel_launches++; c->acc.kernel_ms += ms; c->acc.kernel_bytes += sp.bytes;
+                c->acc.kernel_nvl_bytes += sp.nvl;
+                break;
             case PH_LOCAL: c->acc.local_ops++; c->acc.local_ms += ms; c->acc.local_bytes += sp.bytes; break;
             case PH_NODE: c->acc.node_ops++; c->acc.node_ms += ms; c->acc.node_bytes += sp.bytes; break;
             case PH_WAIT: c->acc.wait_ops++; c->acc.wait_ms += ms; break;

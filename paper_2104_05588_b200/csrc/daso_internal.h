@@ -33,6 +33,8 @@ enum Op : int {
     OP_MERGE = 2,    // Eq. (1)
     OP_PACK = 4,     // wire cast into pack_out
     OP_AVERAGE = 8,  // K4 blocking average
+    OP_NOX = 16,     // peer kernels only: no x stores, no end barrier (blocking batch: the average
+                     // that follows replaces x; launch_avg_publish's end barrier covers the g reads)
 };
 
 struct KernelArgs {
@@ -67,6 +69,9 @@ struct PeerArgs {
     int G = 1, me = 0;
 };
 int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream);
+// Fused-mode blocking tail (Fig. 3 average + Fig. 4 re-publish): x_shard = sum_i wire_f32(slot[i]) / den
+// stored into every node peer's x (pa.xp), then the end barrier (end row of the signal arrays).
+int launch_avg_publish(int wire, const PeerArgs& pa, void* stream);
 
 int set_kernel_impl(int impl);   // returns the previous selection
 int current_kernel_impl();       // 0 register path, 1 TMA-staged path

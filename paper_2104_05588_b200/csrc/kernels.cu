@@ -104,6 +104,55 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
 }
 
 
+// K4 (blocking average) specialised on P <= 4: two 8-parameter chunks per thread, a CTA-width
+// apart (each chunk's warp accesses stay coalesced), with all 2P row loads in flight before the
+// sums.  tools/k4_variants.cu at P = 2 (profiles/r02/k4_variants_u2.txt): 32.8 us vs 36.8 us for one
+// chunk per thread; two contiguous chunks per thread ran 39 us, 512-thread CTAs 36.9, persistent
+// grids 35-42.  Same arithmetic and order as body<OP_AVERAGE> (x = ((0 + s_0) + s_1 ...) / den).
+constexpr int kAvgU = 2;
+template <int WIRE, int P>
+__global__ void __launch_bounds__(kThreads) average_kernel(const KernelArgs a) {
+    const int64_t nchunks = a.n / kVec;
+    const int64_t base = int64_t(blockIdx.x) * kThreads * kAvgU;
+    bool bad = false;
+    if (base + int64_t(kThreads) * kAvgU <= nchunks) {
+        float s[kAvgU][P][kVec];
+#pragma unroll
+        for (int u = 0; u < kAvgU; ++u) {
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                Wire<WIRE>::template load<kVec>(a.slot, p * a.slot_stride + (base + u * kThreads + threadIdx.x) * kVec,
+                                                s[u][p]);
+        }
+#pragma unroll
+        for (int u = 0; u < kAvgU; ++u) {
+            float x[kVec];
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) x[j] = 0.f;
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+#pragma unroll
+                for (int j = 0; j < kVec; ++j) x[j] += s[u][p][j];          // ascending node order (R18)
+            }
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) x[j] = x[j] / a.den;
+            st_f32<kVec>(a.x + (base + u * kThreads + threadIdx.x) * kVec, x);
+#pragma unroll
+            for (int j = 0; j < kVec; ++j) bad |= !isfinite(x[j]);
+        }
+    } else {
+        for (int64_t c = base + threadIdx.x; c < nchunks; c += kThreads) body<OP_AVERAGE, WIRE, kVec>(a, c * kVec, bad);
+    }
+    if (blockIdx.x == gridDim.x - 1) {                           // ragged tail (< 8 elements)
+        const int64_t i = nchunks * kVec + threadIdx.x;
+        if (i < a.n) body<OP_AVERAGE, WIRE, 1>(a, i, bad);
+    }
+    if (a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
+    }
+}
+
 // ----------------------------------------------------------------- TMA-staged variant
 // The same K1/K2/K3 arithmetic with the streams staged through shared memory by the
 // bulk-copy engine (cp.async.bulk, 1-D TMA): one persistent CTA per SM walks its tiles
@@ -265,6 +314,16 @@ int launch_t(const KernelArgs& a, cudaStream_t s) {
     return int(cudaGetLastError());
 }
 
+template <int WIRE, int P>
+int launch_average(const KernelArgs& a, cudaStream_t s) {
+    const int64_t per = int64_t(kThreads) * kAvgU;
+    int64_t blocks = (a.n / kVec + per - 1) / per;
+    if (blocks > 0x7fffffffLL) return launch_t<OP_AVERAGE, WIRE>(a, s);
+    if (blocks < 1) blocks = 1;
+    average_kernel<WIRE, P><<<dim3(unsigned(blocks)), dim3(kThreads), 0, s>>>(a);
+    return int(cudaGetLastError());
+}
+
 // 0 = register (LDG) path everywhere, 1 = TMA-staged path everywhere, 2 = auto (default):
 // the measured-faster path per kernel — register path for the local fused kernels (one-shot
 // grid: ~100% of the copy peak), TMA for the NVLink peer kernel (0.77 vs 0.64 of the link
@@ -323,7 +382,14 @@ int dispatch(int ops, const KernelArgs& a, cudaStream_t s) {
         case OP_UPDATE | OP_MERGE | OP_PACK: return launch_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(a, s);
         case OP_MERGE: return launch_t<OP_MERGE, WIRE>(a, s);
         case OP_MERGE | OP_PACK: return launch_t<OP_MERGE | OP_PACK, WIRE>(a, s);
-        case OP_AVERAGE: return launch_t<OP_AVERAGE, WIRE>(a, s);
+        case OP_AVERAGE:
+            switch (a.P) {
+                case 1: return launch_average<WIRE, 1>(a, s);
+                case 2: return launch_average<WIRE, 2>(a, s);
+                case 3: return launch_average<WIRE, 3>(a, s);
+                case 4: return launch_average<WIRE, 4>(a, s);
+                default: return launch_t<OP_AVERAGE, WIRE>(a, s);
+            }
         case OP_PACK: return launch_t<OP_PACK, WIRE>(a, s);
         default: return int(cudaErrorInvalidValue);
     }

@@ -133,8 +133,10 @@ __device__ __forceinline__ void peer_body(const PeerArgs& pa, int64_t i, bool& b
 #pragma unroll
         for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;
     }
+    if constexpr ((OPS & OP_NOX) == 0) {
 #pragma unroll
-    for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[q] + i, x);
+        for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[q] + i, x);
+    }
 #pragma unroll
     for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
     if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kPeerThreads) peer_kernel(const PeerArgs pa) {
         const unsigned any = __ballot_sync(0xffffffffu, bad);
         if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
     }
-    end_barrier(pa, G);   // 3. end barrier
+    if constexpr ((OPS & OP_NOX) == 0) end_barrier(pa, G);   // 3. end barrier
 }
 
 int peer_blocks_per_sm() {   // grid = SMs x this (DASO_PEER_BPSM, default 2 (measured best)); one-shot if larger
@@ -180,6 +182,78 @@ int launch_peer_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     return int(cudaGetLastError());
 }
 
+
+// ---- fused-mode blocking tail: Fig. 3 average + Fig. 4 re-publish in one kernel.
+// After the blocking group all-gather each rank holds the P packed rows of its shard;
+// x_shard = sum_i wire_f32(slot[i]) / P (ascending node order, R18; K4's arithmetic) is stored
+// straight into every node peer's x over NVLink (the node all-gather), then the end barrier
+// (end row of the signal arrays) makes every shard visible before any rank's next read of x.
+// No start barrier: a peer's x[me-shard] is written only by this rank, and every peer finished
+// its last read of x before it signalled the start barrier of this batch's OP_NOX node-tier
+// kernel, which this rank's node-tier kernel waited for.
+template <int WIRE, int G, int N>
+__device__ __forceinline__ void avg_publish_body(const PeerArgs& pa, int64_t i, bool& bad) {
+    const KernelArgs& a = pa.a;
+    float x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = 0.f;
+#pragma unroll 4
+    for (int p = 0; p < a.P; ++p) {
+        float s[N];
+        Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] += s[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = x[j] / a.den;
+#pragma unroll
+    for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[(pa.me + 1 + q) % G] + i, x);   // next peer first: spread links
+#pragma unroll
+    for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
+}
+
+template <int WIRE, int G>
+__global__ void __launch_bounds__(kPeerThreads) avg_publish_kernel(const PeerArgs pa) {
+    bool bad = false;
+    const int64_t n = pa.a.n;
+    const int64_t nch = n / kPV;
+    const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
+    for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
+        avg_publish_body<WIRE, G, kPV>(pa, c * kPV, bad);
+    if (blockIdx.x == gridDim.x - 1) {
+        const int64_t i = nch * kPV + threadIdx.x;
+        if (i < n) avg_publish_body<WIRE, G, 1>(pa, i, bad);
+    }
+    if (pa.a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
+    }
+    end_barrier(pa, G);
+}
+
+template <int WIRE, int G>
+int launch_avg_publish_t(const PeerArgs& pa, cudaStream_t s, int sms) {
+    const int64_t nch = pa.a.n / kPV;
+    int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
+    avg_publish_kernel<WIRE, G><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
+    return int(cudaGetLastError());
+}
+
+template <int WIRE>
+int dispatch_avg_publish(const PeerArgs& pa, cudaStream_t s, int sms) {
+    switch (pa.G) {
+        case 1: return launch_avg_publish_t<WIRE, 1>(pa, s, sms);
+        case 2: return launch_avg_publish_t<WIRE, 2>(pa, s, sms);
+        case 3: return launch_avg_publish_t<WIRE, 3>(pa, s, sms);
+        case 4: return launch_avg_publish_t<WIRE, 4>(pa, s, sms);
+        case 5: return launch_avg_publish_t<WIRE, 5>(pa, s, sms);
+        case 6: return launch_avg_publish_t<WIRE, 6>(pa, s, sms);
+        case 7: return launch_avg_publish_t<WIRE, 7>(pa, s, sms);
+        case 8: return launch_avg_publish_t<WIRE, 8>(pa, s, sms);
+        default: return int(cudaErrorInvalidValue);
+    }
+}
 
 // ---- TMA-staged variant (daso_kernel_impl(1)): the same batch with the peer gradient
 // loads and the peer parameter stores done by the bulk-copy engine (cp.async.bulk on
@@ -291,7 +365,7 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
         }
-        Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
+        if constexpr ((OPS & OP_NOX) == 0) Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
         Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
         if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
 #pragma unroll
@@ -301,10 +375,12 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
         if (leader) {
             if (k + NS < my) issue_load(k + NS);                         // refill stage s right away
             const int64_t e0 = (int64_t(blockIdx.x) + k * gridDim.x) * kPT;
+            if constexpr ((OPS & OP_NOX) == 0) {
 #pragma unroll
-            for (int q = 0; q < G; ++q) {                                // start with the next peer: spread links
-                const int qq = (pa.me + 1 + q) % G;
-                bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
+                for (int q = 0; q < G; ++q) {                            // start with the next peer: spread links
+                    const int qq = (pa.me + 1 + q) % G;
+                    bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
+                }
             }
             bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
             if constexpr ((OPS & OP_PACK) != 0)
@@ -320,8 +396,10 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
         if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
     }
     // 3. end barrier (all bulk stores of this CTA are complete: wait_group 0 above)
-    if (leader) fence_proxy_async_global();
-    end_barrier(pa, G);
+    if constexpr ((OPS & OP_NOX) == 0) {
+        if (leader) fence_proxy_async_global();
+        end_barrier(pa, G);
+    }
 }
 
 int peer_tma_ctas() {   // DASO_PEER_TMA_CTAS, 0 = default (SMs - 16)
@@ -445,10 +523,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
             if (k + NS < my) issue_load(k + NS);                // stage k % NS consumed: refill it
             unsigned char* ob = outs + size_t(o) * L.out_bytes;
             const int64_t e0 = tile0(k);
+            if constexpr ((OPS & OP_NOX) == 0) {
 #pragma unroll
-            for (int q = 0; q < G; ++q) {
-                const int qq = (pa.me + 1 + q) % G;
-                bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
+                for (int q = 0; q < G; ++q) {
+                    const int qq = (pa.me + 1 + q) % G;
+                    bulk_s2g(pa.xp[qq] + e0, ob + L.ox, kPT * 4);
+                }
             }
             bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
             if constexpr ((OPS & OP_PACK) != 0)
@@ -498,7 +578,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
                 for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
             }
             if (k >= kWsOut && !mbar_wait(&oempty[o], uint32_t(((k / kWsOut) - 1) & 1), pa.err)) break;
-            Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
+            if constexpr ((OPS & OP_NOX) == 0) Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
             Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
             if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
 #pragma unroll
@@ -524,8 +604,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
         }
     }
     // 3. end barrier (the driver has waited for all its bulk stores: wait_group 0)
-    if (tid == kWsCompute) fence_proxy_async_global();
-    end_barrier(pa, G);
+    if constexpr ((OPS & OP_NOX) == 0) {
+        if (tid == kWsCompute) fence_proxy_async_global();
+        end_barrier(pa, G);
+    }
 }
 
 template <int OPS, int WIRE, int G>
@@ -592,6 +674,9 @@ int dispatch_peer(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
         case OP_UPDATE | OP_PACK: return dispatch_g<OP_UPDATE | OP_PACK, WIRE>(pa, s, sms);
         case OP_UPDATE | OP_MERGE: return dispatch_g<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
         case OP_UPDATE | OP_MERGE | OP_PACK: return dispatch_g<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_PACK | OP_NOX: return dispatch_g<OP_UPDATE | OP_PACK | OP_NOX, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_MERGE | OP_PACK | OP_NOX:
+            return dispatch_g<OP_UPDATE | OP_MERGE | OP_PACK | OP_NOX, WIRE>(pa, s, sms);
         default: return int(cudaErrorInvalidValue);
     }
 }
@@ -607,6 +692,17 @@ int launch_peer(int ops, int wire, const PeerArgs& pa, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (wire == DASO_WIRE_BF16) return dispatch_peer<DASO_WIRE_BF16>(ops, pa, s, sms);
     if (wire == DASO_WIRE_FP32) return dispatch_peer<DASO_WIRE_FP32>(ops, pa, s, sms);
+    return int(cudaErrorInvalidValue);
+}
+
+int launch_avg_publish(int wire, const PeerArgs& pa, void* stream) {
+    if (pa.G < 1 || pa.G > kMaxPeers) return int(cudaErrorInvalidValue);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (wire == DASO_WIRE_BF16) return dispatch_avg_publish<DASO_WIRE_BF16>(pa, s, sms);
+    if (wire == DASO_WIRE_FP32) return dispatch_avg_publish<DASO_WIRE_FP32>(pa, s, sms);
     return int(cudaErrorInvalidValue);
 }
 

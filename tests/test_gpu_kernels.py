@@ -138,9 +138,11 @@ def test_merge_fixed_point_is_bitwise():
     np.testing.assert_array_equal(X.cpu().numpy().view(np.uint32), x.view(np.uint32))
 
 
-@pytest.mark.parametrize("n", SIZES)
-@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("n", SIZES + [5003, 2 * 4096 + 4104])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 5, 8])
 def test_k4_average(n, P):
+    """P <= 4 runs the P-specialised two-chunk kernel (5003 and 12296: full CTAs then a partial CTA
+    and the ragged tail), P > 4 the generic body."""
     stride = (n + 63) // 64 * 64
     rows, slot = bf16_rows(P, n, stride, 80)
     X = torch.zeros(n, dtype=torch.float32, device="cuda")
