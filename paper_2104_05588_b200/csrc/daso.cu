@@ -218,7 +218,9 @@ double kernel_bytes_per_elem(int ops, int P, double wb) {
 }
 
 int launch(daso_ctx* c, int ops, const daso::KernelArgs& a, cudaStream_t s) {
-    Span sp(c, s, PH_KERNEL, kernel_bytes_per_elem(ops, a.P, double(c->wire_bytes)) * double(a.n));
+    // NVLink bytes per direction of a kernel push (blocking sync, below): the packed row to each member
+    Span sp(c, s, PH_KERNEL, kernel_bytes_per_elem(ops, a.P, double(c->wire_bytes)) * double(a.n),
+            double(a.npush) * double(c->wire_bytes) * double(a.n));
     return daso::launch_fused(ops, c->cfg.wire, a, s);
 }
 
@@ -298,6 +300,49 @@ daso_status push_exchange(daso_ctx* c, cudaStream_t s) {
                                   c->side));
     }
     CUDA_TRY(c, cudaEventRecord(c->ev_exchanged, c->side));
+    return DASO_OK;
+}
+
+// ---- kernel push (blocking syncs, copy-engine transport) ---------------------------------
+// In a blocking batch (Fig. 3) the exchange is on the critical path.  With the CE transport's
+// IPC mappings of the group members' slots in place, the update + pack kernel stores the packed row
+// straight into row `node` of every member's slot over NVLink (one pass, no separate copy phase);
+// the same flow control and arrival flags as the copy-engine pushes, issued on the compute stream:
+// before the kernel, wait until every member has consumed exchange e-1 (its row `node` is free);
+// after it, raise the arrival flag e in every member's xs (cuStreamWriteValue64 orders it after the
+// kernel's stores).  Not in a batch that also merges: there this rank's acknowledgement of e-1
+// follows the kernel, and the members wait for it before their own kernel pushes.
+// DASO_BLOCKING_PUSH=0 keeps the copy-engine pushes (A/B).
+bool kernel_push_enabled() {   // read per blocking batch, so a test can compare both transports
+    const char* e = getenv("DASO_BLOCKING_PUSH");
+    return !(e && strcmp(e, "0") == 0);
+}
+
+bool kernel_push_ok(daso_ctx* c, bool merge) {
+    return c->ce && c->exch_enabled && !merge && c->P > 1 && c->P - 1 <= daso::kMaxPush && kernel_push_enabled();
+}
+
+daso_status kernel_push_prepare(daso_ctx* c, daso::KernelArgs& a, cudaStream_t s) {
+    const unsigned long long e = ++c->exch_epoch;
+    const size_t row = size_t(c->seg) * c->wire_bytes;
+    Span sp(c, s, PH_WAIT, 0.0);
+    a.npush = 0;
+    for (int k = 1; k < c->P; ++k) {
+        const int i = (c->node + k) % c->P;
+        if (wait_value64()(s, CUdeviceptr(c->xs + c->P + i), e - 1, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return c->fail(DASO_ERR_CUDA, "cuStreamWaitValue64 (exchange flow control) failed");
+        a.push[a.npush++] = static_cast<char*>(c->peer_slot[i]) + size_t(c->node) * row;
+    }
+    return DASO_OK;
+}
+
+daso_status kernel_push_publish(daso_ctx* c, cudaStream_t s) {
+    for (int k = 1; k < c->P; ++k) {
+        const int i = (c->node + k) % c->P;
+        if (write_value64()(s, CUdeviceptr(c->peer_xs[i] + c->node), c->exch_epoch, 0) != CUDA_SUCCESS)
+            return c->fail(DASO_ERR_CUDA, "cuStreamWriteValue64 (exchange flag) failed");
+    }
+    CUDA_TRY(c, cudaEventRecord(c->ev_exchanged, s));   // wait_exchange's event wait: already in order
     return DASO_OK;
 }
 
@@ -492,14 +537,20 @@ daso_status step_sharded(daso_ctx* c, const daso_record& r, float lr, cudaStream
         a.den = float(2 * r.merge_S + c->P);
         c->inflight = false;
     }
+    bool kpush = false;
     if (send) {
         ops |= daso::OP_PACK;
         a.pack_out = own_segment(c);
+        if (r.blocking && kernel_push_ok(c, merge)) {
+            STATUS_TRY(kernel_push_prepare(c, a, s));
+            ops |= daso::OP_PUSH;
+            kpush = true;
+        }
     }
     KERN_TRY(c, launch(c, ops, a, s));
     if (merge) STATUS_TRY(exchange_consumed(c, s));
     if (send) {
-        STATUS_TRY(start_exchange(c, s));
+        STATUS_TRY(kpush ? kernel_push_publish(c, s) : start_exchange(c, s));
         if (r.blocking) {
             if (c->vc) {   // G == 1 in a virtual cluster: nothing follows the tail
                 c->vc_blocking = true;
@@ -543,6 +594,11 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
         // packs (no x stores to the peers, no end barrier: the tail's end barrier covers it)
         if (r.blocking) ops |= daso::OP_NOX;
     }
+    const bool kpush = send && r.blocking && kernel_push_ok(c, merge);
+    if (kpush) {
+        STATUS_TRY(kernel_push_prepare(c, pa.a, s));
+        ops |= daso::OP_PUSH;
+    }
     {
         // HBM bytes on THIS GPU per shard element: own x r + w, v r + w, own g r
         // (20) + the G-1 peers reading this GPU's g and writing its x (8 (G-1)) + slot rows / pack.
@@ -550,13 +606,14 @@ daso_status step_fused(daso_ctx* c, const daso_record& r, float lr, cudaStream_t
         const double wb = double(c->wire_bytes);
         double per = ((ops & daso::OP_NOX) ? 16.0 + 4.0 * (c->G - 1) : 20.0 + 8.0 * (c->G - 1)) +
                      ((ops & daso::OP_MERGE) ? c->P * wb : 0) + ((ops & daso::OP_PACK) ? wb : 0);
-        const double nvl = ((ops & daso::OP_NOX) ? 1.0 : 2.0) * 4.0 * (c->G - 1) * double(sh);
+        const double nvl = ((ops & daso::OP_NOX) ? 1.0 : 2.0) * 4.0 * (c->G - 1) * double(sh) +
+                           double(pa.a.npush) * wb * double(sh);
         Span sp(c, s, PH_KERNEL, per * double(sh), nvl);
         KERN_TRY(c, daso::launch_peer(ops, c->cfg.wire, pa, s));
     }
     if (merge) STATUS_TRY(exchange_consumed(c, s));
     if (send) {
-        STATUS_TRY(start_exchange(c, s));
+        STATUS_TRY(kpush ? kernel_push_publish(c, s) : start_exchange(c, s));
         if (r.blocking) {
             if (c->vc) {
                 c->vc_blocking = true;

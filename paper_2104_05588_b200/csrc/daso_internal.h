@@ -35,6 +35,7 @@ enum Op : int {
     OP_AVERAGE = 8,  // K4 blocking average
     OP_NOX = 16,     // peer kernels only: no x stores, no end barrier (blocking batch: the average
                      // that follows replaces x; launch_avg_publish's end barrier covers the g reads)
+    OP_PUSH = 32,    // with OP_PACK: also store the packed row into KernelArgs::push[0..npush) (kernel push)
 };
 
 struct KernelArgs {
@@ -48,10 +49,15 @@ struct KernelArgs {
     int P = 0;
     float den = 1.f;              // 2S + P (merge) or P (average)
     void* pack_out = nullptr;
+    // blocking sync with the copy-engine transport: the packed row is also stored into these
+    // npush remote slot rows (group members' slots over NVLink) by the same kernel
+    void* push[7] = {};
+    int npush = 0;
     uint32_t* flag = nullptr;     // bit 0: non-finite parameter (nullable: check off)
     uint32_t* err = nullptr;      // bit 2: TMA (mbarrier) wait timed out (nullable)
 };
 
+constexpr int kMaxPush = 7;   // KernelArgs::push capacity (groups of up to 8 members)
 int launch_fused(int ops, int wire, const KernelArgs& a, void* stream);
 
 // fused node-local tier over NVLink peer memory (peer.cu)

@@ -28,9 +28,17 @@ namespace {
 using namespace dev;
 
 // ----------------------------------------------------------------- fused body
-template <int OPS, int WIRE, int N>
+// PN > 0: the number of slot rows P is a compile-time constant and the P row loads of a merge are
+// issued with the x, v, g loads at the top (the runtime-P loop below cannot hoist them above the v
+// store, since the pointers may alias, so they would start a second round trip to HBM).
+template <int OPS, int WIRE, int N, int PN = 0>
 __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) {
     float x[N];
+    float sp[PN > 0 ? PN : 1][N];
+    if constexpr (PN > 0 && (OPS & OP_MERGE) != 0) {
+#pragma unroll
+        for (int p = 0; p < PN; ++p) Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, sp[p]);
+    }
     if constexpr ((OPS & (OP_UPDATE | OP_MERGE | OP_PACK)) != 0) ld_f32<N>(a.x + i, x);
     if constexpr ((OPS & OP_UPDATE) != 0) {
         float v[N], g[N];
@@ -48,12 +56,20 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
         float acc[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) acc[j] = 0.f;
-#pragma unroll 4
-        for (int p = 0; p < a.P; ++p) {                          // ascending node order (R18)
-            float s[N];
-            Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
+        if constexpr (PN > 0) {
 #pragma unroll
-            for (int j = 0; j < N; ++j) acc[j] += s[j] - x[j];
+            for (int p = 0; p < PN; ++p) {                       // ascending node order (R18)
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[j] += sp[p][j] - x[j];
+            }
+        } else {
+#pragma unroll 4
+            for (int p = 0; p < a.P; ++p) {                      // ascending node order (R18)
+                float s[N];
+                Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[j] += s[j] - x[j];
+            }
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) x[j] = x[j] + acc[j] / a.den;   // (2S x + sum s)/(2S+P), delta form
@@ -76,7 +92,14 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
 #pragma unroll
         for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
     }
-    if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
+    if constexpr ((OPS & OP_PACK) != 0) {
+        Wire<WIRE>::template store<N>(a.pack_out, i, x);
+        if constexpr ((OPS & OP_PUSH) != 0) {   // group members' slots (a separate instantiation: the
+#pragma unroll                                        // push code costs the plain pack kernels registers)
+            for (int k = 0; k < kMaxPush; ++k)
+                if (k < a.npush) Wire<WIRE>::template store<N>(a.push[k], i, x);
+        }
+    }
 }
 
 // Eight parameters per thread for every op set.  Measured alternatives (profiles/r01): 32 per
@@ -86,13 +109,13 @@ __device__ __forceinline__ void body(const KernelArgs& a, int64_t i, bool& bad) 
 // store, persistent CTAs) 97.4 us (profiles/r02/k4_variants.txt); and
 // issuing the two 128-bit loads of a stream from an array loop instead of two named loads cost K1
 // 9 % (75 -> 82 us, same box, A/B in one run): ptxas schedules the explicit form better.
-template <int OPS, int WIRE>
+template <int OPS, int WIRE, int PN = 0>
 __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
     const int64_t nchunks = a.n / kVec;
     const int64_t stride = int64_t(gridDim.x) * kThreads;
     bool bad = false;
     for (int64_t c = int64_t(blockIdx.x) * kThreads + threadIdx.x; c < nchunks; c += stride)
-        body<OPS, WIRE, kVec>(a, c * kVec, bad);
+        body<OPS, WIRE, kVec, PN>(a, c * kVec, bad);
     if (blockIdx.x == gridDim.x - 1) {                           // ragged tail (< 8 elements)
         const int64_t i = nchunks * kVec + threadIdx.x;
         if (i < a.n) body<OPS, WIRE, 1>(a, i, bad);
@@ -106,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(const KernelArgs a) {
 
 // K4 (blocking average) specialised on P <= 4: two 8-parameter chunks per thread, a CTA-width
 // apart (each chunk's warp accesses stay coalesced), with all 2P row loads in flight before the
-// sums.  tools/k4_variants.cu at P = 2 (profiles/r02/k4_variants_u2.txt): 32.8 us vs 36.8 us for one
+// sums.  tools/k4_variants.cu at P = 2 (profiles/r02/one_n/k4_variants*.jsonl): 32.8 us vs 36.8 us for one
 // chunk per thread; two contiguous chunks per thread ran 39 us, 512-thread CTAs 36.9, persistent
 // grids 35-42.  Same arithmetic and order as body<OP_AVERAGE> (x = ((0 + s_0) + s_1 ...) / den).
 constexpr int kAvgU = 2;
@@ -301,7 +324,7 @@ int sm_count() {
     return cached_sms > 0 ? cached_sms : 148;
 }
 
-template <int OPS, int WIRE>
+template <int OPS, int WIRE, int PN = 0>
 int launch_t(const KernelArgs& a, cudaStream_t s) {
     // One 8-parameter chunk per thread ("one-shot" grid): measured 95% of the copy
     // peak for K1 on B200 vs 82% for a persistent grid-stride grid of SMs x occupancy
@@ -310,8 +333,20 @@ int launch_t(const KernelArgs& a, cudaStream_t s) {
     int64_t blocks = (nchunks + kThreads - 1) / kThreads;
     if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;
     if (blocks < 1) blocks = 1;
-    fused_kernel<OPS, WIRE><<<dim3(unsigned(blocks)), dim3(kThreads), 0, s>>>(a);
+    fused_kernel<OPS, WIRE, PN><<<dim3(unsigned(blocks)), dim3(kThreads), 0, s>>>(a);
     return int(cudaGetLastError());
+}
+
+// K3 with the P slot-row loads issued up front for P <= 4 (the 2x4 / 4x2 / 2x2 topologies)
+template <int OPS, int WIRE>
+int launch_merge(const KernelArgs& a, cudaStream_t s) {
+    switch (a.P) {
+        case 1: return launch_t<OPS, WIRE, 1>(a, s);
+        case 2: return launch_t<OPS, WIRE, 2>(a, s);
+        case 3: return launch_t<OPS, WIRE, 3>(a, s);
+        case 4: return launch_t<OPS, WIRE, 4>(a, s);
+        default: return launch_t<OPS, WIRE>(a, s);
+    }
 }
 
 template <int WIRE, int P>
@@ -366,7 +401,7 @@ bool tma_ok(const KernelArgs& a, int wb) {
 template <int WIRE>
 int dispatch(int ops, const KernelArgs& a, cudaStream_t s) {
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
-    if (kernel_impl() == 1 && tma_ok(a, wb)) {
+    if (kernel_impl() == 1 && tma_ok(a, wb) && a.npush == 0) {
         switch (ops) {
             case OP_UPDATE: return launch_tma<OP_UPDATE, WIRE>(a, s);
             case OP_UPDATE | OP_PACK: return launch_tma<OP_UPDATE | OP_PACK, WIRE>(a, s);
@@ -378,8 +413,9 @@ int dispatch(int ops, const KernelArgs& a, cudaStream_t s) {
     switch (ops) {
         case OP_UPDATE: return launch_t<OP_UPDATE, WIRE>(a, s);
         case OP_UPDATE | OP_PACK: return launch_t<OP_UPDATE | OP_PACK, WIRE>(a, s);
-        case OP_UPDATE | OP_MERGE: return launch_t<OP_UPDATE | OP_MERGE, WIRE>(a, s);
-        case OP_UPDATE | OP_MERGE | OP_PACK: return launch_t<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(a, s);
+        case OP_UPDATE | OP_PACK | OP_PUSH: return launch_t<OP_UPDATE | OP_PACK | OP_PUSH, WIRE>(a, s);
+        case OP_UPDATE | OP_MERGE: return launch_merge<OP_UPDATE | OP_MERGE, WIRE>(a, s);
+        case OP_UPDATE | OP_MERGE | OP_PACK: return launch_merge<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(a, s);
         case OP_MERGE: return launch_t<OP_MERGE, WIRE>(a, s);
         case OP_MERGE | OP_PACK: return launch_t<OP_MERGE | OP_PACK, WIRE>(a, s);
         case OP_AVERAGE:

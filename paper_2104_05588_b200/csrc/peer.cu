@@ -139,7 +139,14 @@ __device__ __forceinline__ void peer_body(const PeerArgs& pa, int64_t i, bool& b
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
-    if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store<N>(a.pack_out, i, x);
+    if constexpr ((OPS & OP_PACK) != 0) {
+        Wire<WIRE>::template store<N>(a.pack_out, i, x);
+        if constexpr ((OPS & OP_PUSH) != 0) {   // group members' slots (a separate instantiation: the
+#pragma unroll                                        // push code costs the plain pack kernels registers)
+            for (int k = 0; k < kMaxPush; ++k)
+                if (k < a.npush) Wire<WIRE>::template store<N>(a.push[k], i, x);
+        }
+    }
 }
 
 template <int OPS, int WIRE, int G>
@@ -383,8 +390,15 @@ __global__ void __launch_bounds__(kPeerThreads, 1) peer_tma_kernel(const PeerArg
                 }
             }
             bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
-            if constexpr ((OPS & OP_PACK) != 0)
+            if constexpr ((OPS & OP_PACK) != 0) {
                 bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, ob + L.opack, kPT * wb);
+                if constexpr ((OPS & OP_PUSH) != 0) {
+#pragma unroll
+                    for (int k = 0; k < kMaxPush; ++k)                  // group members' slots (kernel push)
+                        if (k < a.npush)
+                            bulk_s2g(static_cast<unsigned char*>(a.push[k]) + e0 * wb, ob + L.opack, kPT * wb);
+                }
+            }
             bulk_commit();
         }
     }
@@ -531,8 +545,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
                 }
             }
             bulk_s2g(a.v + e0, ob + L.ov, kPT * 4);
-            if constexpr ((OPS & OP_PACK) != 0)
+            if constexpr ((OPS & OP_PACK) != 0) {
                 bulk_s2g(static_cast<unsigned char*>(a.pack_out) + e0 * wb, ob + L.opack, kPT * wb);
+                if constexpr ((OPS & OP_PUSH) != 0) {
+#pragma unroll
+                    for (int k = 0; k < kMaxPush; ++k)                  // group members' slots (kernel push)
+                        if (k < a.npush)
+                            bulk_s2g(static_cast<unsigned char*>(a.push[k]) + e0 * wb, ob + L.opack, kPT * wb);
+                }
+            }
             bulk_commit();
             if (k >= 1) {                                       // the previous tile's buffer has been read
                 bulk_wait_read<1>();
@@ -640,10 +661,17 @@ int peer_path() {
     return v;
 }
 
+uintptr_t push_bits(const KernelArgs& a) {
+    uintptr_t b = 0;
+    for (int k = 0; k < a.npush; ++k) b |= reinterpret_cast<uintptr_t>(a.push[k]);
+    return b;
+}
+
 template <int OPS, int WIRE, int G>
 int launch_peer_any(const PeerArgs& pa, cudaStream_t s, int sms) {
     const bool al = ((reinterpret_cast<uintptr_t>(pa.a.x) | reinterpret_cast<uintptr_t>(pa.a.v) |
-                      reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot)) & 15u) == 0;
+                      reinterpret_cast<uintptr_t>(pa.a.pack_out) | reinterpret_cast<uintptr_t>(pa.a.slot) |
+                      push_bits(pa.a)) & 15u) == 0;
     // TMA unless the register path is forced (daso_kernel_impl(0))
     const int impl = current_kernel_impl();   // 0 register, 1 TMA, 2 auto (DASO_PEER, default ws)
     const int path = impl == 2 ? peer_path() : impl == 1 ? 1 : 0;
@@ -675,6 +703,8 @@ int dispatch_peer(int ops, const PeerArgs& pa, cudaStream_t s, int sms) {
         case OP_UPDATE | OP_MERGE: return dispatch_g<OP_UPDATE | OP_MERGE, WIRE>(pa, s, sms);
         case OP_UPDATE | OP_MERGE | OP_PACK: return dispatch_g<OP_UPDATE | OP_MERGE | OP_PACK, WIRE>(pa, s, sms);
         case OP_UPDATE | OP_PACK | OP_NOX: return dispatch_g<OP_UPDATE | OP_PACK | OP_NOX, WIRE>(pa, s, sms);
+        case OP_UPDATE | OP_PACK | OP_NOX | OP_PUSH:
+            return dispatch_g<OP_UPDATE | OP_PACK | OP_NOX | OP_PUSH, WIRE>(pa, s, sms);
         case OP_UPDATE | OP_MERGE | OP_PACK | OP_NOX:
             return dispatch_g<OP_UPDATE | OP_MERGE | OP_PACK | OP_NOX, WIRE>(pa, s, sms);
         default: return int(cudaErrorInvalidValue);

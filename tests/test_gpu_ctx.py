@@ -69,6 +69,7 @@ def test_trace_counts_and_bytes():
     t = c.trace_read()
     assert t["steps"] == 8 and t["kernel_launches"] == 8
     assert t["kernel_bytes"] == 8 * 20 * n            # K1 at 1x1: 20 B/param
+    assert t["kernel_nvl_bytes"] == 0                  # no node tier at G = 1
     assert t["kernel_ms"] > 0 and t["local_ops"] == 0 and t["exch_ops"] == 0
     c.finalize()
 

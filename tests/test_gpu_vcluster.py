@@ -122,7 +122,8 @@ def test_vcluster_one_gpu_per_node_modes(P, mode):
 
 
 @pytest.mark.parametrize("P,G,B,S,mode", [(2, 2, 4, 1, "fused"), (2, 4, 4, 1, "fused"), (4, 2, 4, 1, "fused"),
-                                          (8, 1, 4, 1, "fused"), (2, 2, 2, 2, "fused"), (4, 1, 2, 2, "faithful")])
+                                          (8, 1, 4, 1, "fused"), (2, 2, 2, 2, "fused"), (4, 1, 2, 2, "faithful"),
+                                          (2, 2, 1, 0, "fused"), (4, 1, 1, 0, "fused")])
 @pytest.mark.parametrize("wire", ["bf16", "fp32"])
 def test_vcluster_copy_engine_exchange(P, G, B, S, mode, wire):
     """The global tier's copy-engine exchange (DASO_EXCH_CE, the bench default) for real, between the
@@ -195,3 +196,53 @@ def test_vcluster_full_size_2x4_sampled(wire):
         for l in range(1, G):
             for k in range(steps):
                 np.testing.assert_array_equal(trace[j * G + l][k], trace[j * G][k])
+
+
+@pytest.mark.parametrize("P,G", [(2, 2), (2, 4)])
+def test_vcluster_fused_trace_accounting(P, G):
+    """The library's per-launch byte accounting (daso_trace) for the fused node tier: a plain batch is
+    one node-tier launch moving 2 (G-1) * 4 B per shard element over NVLink per direction (peer
+    gradient reads + peer parameter stores); a blocking batch is the node-tier kernel without its
+    parameter stores (OP_NOX, gradient reads only) plus the average/re-publish launch (stores only),
+    so the same NVLink bytes over two launches.  (Fig. 3 / Fig. 4.)"""
+    torch.cuda.set_device(0)
+    d = 4099
+    seg = daso.daso_padded_numel(d, G) // G
+    per_batch = 2.0 * (G - 1) * 4.0 * seg
+    # (B, S, exchange, launches per batch, extra NVLink bytes per batch): with the copy-engine transport
+    # a blocking batch's node-tier kernel also stores the packed bf16 row into the P-1 other group
+    # members' slots (kernel push), 2 B per shard element each
+    for B, S, ex, launches, extra in [(4, 1, "nccl", 1, 0.0), (1, 0, "nccl", 2, 0.0),
+                                      (1, 0, "ce", 2, (P - 1) * 2.0 * seg)]:
+        vc = daso.VCluster(P * G, G, B, S, d, total_epochs=1, steps_per_epoch=B * 64, mode="fused", exchange=ex)
+        try:
+            for r in range(P * G):
+                vc.rank(r).trace_enable(True)
+            steps = 3
+            for k in range(steps):
+                for r in range(P * G):
+                    vc.g(r)[:d] = torch.from_numpy(synthetic.microbench_grad(d, r, k)).cuda()
+                vc.step(0.01)
+            for r in range(P * G):
+                t = vc.rank(r).trace_read(reset=True)
+                assert t["kernel_launches"] == steps * launches, (B, S, ex, r, t)
+                assert t["kernel_nvl_bytes"] == pytest.approx(steps * (per_batch + extra)), (B, S, ex, r, t)
+                assert vc.rank(r).check_finite()
+        finally:
+            vc.destroy()
+
+
+@pytest.mark.parametrize("P,G", [(2, 2), (4, 1), (2, 4), (8, 1)])
+def test_vcluster_blocking_kernel_push_equals_copy_engines(P, G, monkeypatch):
+    """Blocking syncs with the CE transport: the pack kernel storing the packed row into every group
+    member's slot (kernel push, default) and the copy-engine pushes after it (DASO_BLOCKING_PUSH=0)
+    deliver the same rows, so every rank's trajectory is bitwise identical (Fig. 3)."""
+    kw = dict(steps=24, warm=1, cool=1, epochs=3, spe=8, flags="1", wire="bf16", exchange="ce")
+    monkeypatch.setenv("DASO_BLOCKING_PUSH", "0")
+    ce, recs_ce = run_vc(P, G, 4, 1, **kw)
+    monkeypatch.setenv("DASO_BLOCKING_PUSH", "1")
+    kp, recs_kp = run_vc(P, G, 4, 1, **kw)
+    assert recs_ce == recs_kp
+    for r in range(P * G):
+        for k in range(len(ce[r])):
+            np.testing.assert_array_equal(ce[r][k].view(np.uint32), kp[r][k].view(np.uint32))

@@ -22,12 +22,17 @@ def main():
     ap.add_argument("--topology", default="1x2")
     ap.add_argument("--n", type=int, default=25_557_032)
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--B", type=int, default=4)
+    ap.add_argument("--S", type=int, default=1, help="S = 0 with B = 1: every batch a blocking sync (OP_NOX "
+                    "node-tier kernel + average/re-publish kernel)")
+    ap.add_argument("--exchange", choices=["nccl", "ce"], default="nccl")
     a = ap.parse_args()
     import torch
     import paper_2104_05588_b200 as daso
     P, G = (int(v) for v in a.topology.split("x"))
     torch.cuda.set_device(0)
-    vc = daso.VCluster(P * G, G, 4, 1, a.n, total_epochs=1, steps_per_epoch=4 << 20, mode="fused")
+    vc = daso.VCluster(P * G, G, a.B, a.S, a.n, total_epochs=1, steps_per_epoch=max(a.B, 1) << 20, mode="fused",
+                       exchange=a.exchange)
     gen = torch.Generator(device="cuda").manual_seed(0)
     x0 = torch.randn(a.n, device="cuda", generator=gen) * 0.02
     for r in range(P * G):
@@ -43,7 +48,7 @@ def main():
     k = sum(t["kernel_launches"] for t in tr)
     ms = sum(t["kernel_ms"] for t in tr)
     by = sum(t["kernel_bytes"] for t in tr)
-    print(json.dumps({"topology": a.topology, "n": a.n, "launches": k, "us_per_launch": ms / max(k, 1) * 1e3,
+    print(json.dumps({"topology": a.topology, "B": a.B, "S": a.S, "exchange": a.exchange, "n": a.n, "launches": k, "us_per_launch": ms / max(k, 1) * 1e3,
                       "hbm_bytes_per_launch": by / max(k, 1), "hbm_gbs": by / (ms * 1e-3) / 1e9 if ms else None}))
 
 
