@@ -199,7 +199,7 @@ def test_vcluster_full_size_2x4_sampled(wire):
 
 
 @pytest.mark.parametrize("P,G", [(2, 2), (2, 4)])
-def test_vcluster_fused_trace_accounting(P, G):
+def test_vcluster_fused_trace_accounting(P, G, monkeypatch):
     """The library's per-launch byte accounting (daso_trace) for the fused node tier: a plain batch is
     one node-tier launch moving 2 (G-1) * 4 B per shard element over NVLink per direction (peer
     gradient reads + peer parameter stores); a blocking batch is the node-tier kernel without its
@@ -211,9 +211,11 @@ def test_vcluster_fused_trace_accounting(P, G):
     per_batch = 2.0 * (G - 1) * 4.0 * seg
     # (B, S, exchange, launches per batch, extra NVLink bytes per batch): with the copy-engine transport
     # a blocking batch's node-tier kernel also stores the packed bf16 row into the P-1 other group
-    # members' slots (kernel push), 2 B per shard element each
-    for B, S, ex, launches, extra in [(4, 1, "nccl", 1, 0.0), (1, 0, "nccl", 2, 0.0),
-                                      (1, 0, "ce", 2, (P - 1) * 2.0 * seg)]:
+    # members' slots (kernel push, DASO_BLOCKING_PUSH=2), 2 B per shard element each; with the default (1)
+    # the copy engines push after the kernel (exchange bytes, not kernel bytes)
+    for B, S, ex, mode, launches, extra in [(4, 1, "nccl", "1", 1, 0.0), (1, 0, "nccl", "1", 2, 0.0),
+                                            (1, 0, "ce", "2", 2, (P - 1) * 2.0 * seg), (1, 0, "ce", "1", 2, 0.0)]:
+        monkeypatch.setenv("DASO_BLOCKING_PUSH", mode)
         vc = daso.VCluster(P * G, G, B, S, d, total_epochs=1, steps_per_epoch=B * 64, mode="fused", exchange=ex)
         try:
             for r in range(P * G):
@@ -225,8 +227,8 @@ def test_vcluster_fused_trace_accounting(P, G):
                 vc.step(0.01)
             for r in range(P * G):
                 t = vc.rank(r).trace_read(reset=True)
-                assert t["kernel_launches"] == steps * launches, (B, S, ex, r, t)
-                assert t["kernel_nvl_bytes"] == pytest.approx(steps * (per_batch + extra)), (B, S, ex, r, t)
+                assert t["kernel_launches"] == steps * launches, (B, S, ex, mode, r, t)
+                assert t["kernel_nvl_bytes"] == pytest.approx(steps * (per_batch + extra)), (B, S, ex, mode, r, t)
                 assert vc.rank(r).check_finite()
         finally:
             vc.destroy()
@@ -235,12 +237,13 @@ def test_vcluster_fused_trace_accounting(P, G):
 @pytest.mark.parametrize("P,G", [(2, 2), (4, 1), (2, 4), (8, 1)])
 def test_vcluster_blocking_kernel_push_equals_copy_engines(P, G, monkeypatch):
     """Blocking syncs with the CE transport: the pack kernel storing the packed row into every group
-    member's slot (kernel push, default) and the copy-engine pushes after it (DASO_BLOCKING_PUSH=0)
-    deliver the same rows, so every rank's trajectory is bitwise identical (Fig. 3)."""
+    member's slot (kernel push; DASO_BLOCKING_PUSH=2 also from the fused node-tier kernel at G > 1) and
+    the copy-engine pushes after it (DASO_BLOCKING_PUSH=0) deliver the same rows, so every rank's
+    trajectory is bitwise identical (Fig. 3)."""
     kw = dict(steps=24, warm=1, cool=1, epochs=3, spe=8, flags="1", wire="bf16", exchange="ce")
     monkeypatch.setenv("DASO_BLOCKING_PUSH", "0")
     ce, recs_ce = run_vc(P, G, 4, 1, **kw)
-    monkeypatch.setenv("DASO_BLOCKING_PUSH", "1")
+    monkeypatch.setenv("DASO_BLOCKING_PUSH", "2")
     kp, recs_kp = run_vc(P, G, 4, 1, **kw)
     assert recs_ce == recs_kp
     for r in range(P * G):
