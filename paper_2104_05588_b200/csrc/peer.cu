@@ -190,78 +190,6 @@ int launch_peer_t(const PeerArgs& pa, cudaStream_t s, int sms) {
 }
 
 
-// ---- fused-mode blocking tail: Fig. 3 average + Fig. 4 re-publish in one kernel.
-// After the blocking group all-gather (P:86) each rank holds the P packed rows of its shard;
-// x_shard = sum_i wire_f32(slot[i]) / P (ascending node order, R18; K4's arithmetic) is stored
-// straight into every node peer's x over NVLink (the node all-gather), then the end barrier
-// (end row of the signal arrays) makes every shard visible before any rank's next read of x.
-// No start barrier: a peer's x[me-shard] is written only by this rank, and every peer finished
-// its last read of x before it signalled the start barrier of this batch's OP_NOX node-tier
-// kernel, which this rank's node-tier kernel waited for.
-template <int WIRE, int G, int N>
-__device__ __forceinline__ void avg_publish_body(const PeerArgs& pa, int64_t i, bool& bad) {
-    const KernelArgs& a = pa.a;
-    float x[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) x[j] = 0.f;
-#pragma unroll 4
-    for (int p = 0; p < a.P; ++p) {
-        float s[N];
-        Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
-#pragma unroll
-        for (int j = 0; j < N; ++j) x[j] += s[j];
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) x[j] = x[j] / a.den;
-#pragma unroll
-    for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[(pa.me + 1 + q) % G] + i, x);   // next peer first: spread links
-#pragma unroll
-    for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
-}
-
-template <int WIRE, int G>
-__global__ void __launch_bounds__(kPeerThreads) avg_publish_kernel(const PeerArgs pa) {
-    bool bad = false;
-    const int64_t n = pa.a.n;
-    const int64_t nch = n / kPV;
-    const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
-    for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
-        avg_publish_body<WIRE, G, kPV>(pa, c * kPV, bad);
-    if (blockIdx.x == gridDim.x - 1) {
-        const int64_t i = nch * kPV + threadIdx.x;
-        if (i < n) avg_publish_body<WIRE, G, 1>(pa, i, bad);
-    }
-    if (pa.a.flag != nullptr) {
-        const unsigned any = __ballot_sync(0xffffffffu, bad);
-        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
-    }
-    end_barrier(pa, G);
-}
-
-template <int WIRE, int G>
-int launch_avg_publish_t(const PeerArgs& pa, cudaStream_t s, int sms) {
-    const int64_t nch = pa.a.n / kPV;
-    int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
-    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
-    avg_publish_kernel<WIRE, G><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
-    return int(cudaGetLastError());
-}
-
-template <int WIRE>
-int dispatch_avg_publish(const PeerArgs& pa, cudaStream_t s, int sms) {
-    switch (pa.G) {
-        case 1: return launch_avg_publish_t<WIRE, 1>(pa, s, sms);
-        case 2: return launch_avg_publish_t<WIRE, 2>(pa, s, sms);
-        case 3: return launch_avg_publish_t<WIRE, 3>(pa, s, sms);
-        case 4: return launch_avg_publish_t<WIRE, 4>(pa, s, sms);
-        case 5: return launch_avg_publish_t<WIRE, 5>(pa, s, sms);
-        case 6: return launch_avg_publish_t<WIRE, 6>(pa, s, sms);
-        case 7: return launch_avg_publish_t<WIRE, 7>(pa, s, sms);
-        case 8: return launch_avg_publish_t<WIRE, 8>(pa, s, sms);
-        default: return int(cudaErrorInvalidValue);
-    }
-}
-
 // ---- TMA-staged variant (daso_kernel_impl(1)): the same batch with the peer gradient
 // loads and the peer parameter stores done by the bulk-copy engine (cp.async.bulk on
 // NVLink-mapped global addresses) through an mbarrier ring of shared-memory stages, one
@@ -649,6 +577,146 @@ int launch_peer_ws_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     const int grid = peer_tma_ctas() > 0 ? std::min(peer_tma_ctas(), sms) : std::max(1, sms - 16);
     peer_ws_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kWsThreads), smem, s>>>(pa, NS);
     return int(cudaGetLastError());
+}
+
+// ---- fused-mode blocking tail: Fig. 3 average + Fig. 4 re-publish in one kernel.
+// After the blocking group all-gather (P:86) each rank holds the P packed rows of its shard;
+// x_shard = sum_i wire_f32(slot[i]) / P (ascending node order, R18; K4's arithmetic) is stored
+// straight into every node peer's x over NVLink (the node all-gather), then the end barrier
+// (end row of the signal arrays) makes every shard visible before any rank's next read of x.
+// No start barrier: a peer's x[me-shard] is written only by this rank, and every peer finished
+// its last read of x before it signalled the start barrier of this batch's OP_NOX node-tier
+// kernel, which this rank's node-tier kernel waited for.
+template <int WIRE, int G, int N>
+__device__ __forceinline__ void avg_publish_body(const PeerArgs& pa, int64_t i, bool& bad) {
+    const KernelArgs& a = pa.a;
+    float x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = 0.f;
+#pragma unroll 4
+    for (int p = 0; p < a.P; ++p) {
+        float s[N];
+        Wire<WIRE>::template load<N>(a.slot, p * a.slot_stride + i, s);
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] += s[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = x[j] / a.den;
+#pragma unroll
+    for (int q = 0; q < G; ++q) st_f32<N>(pa.xp[(pa.me + 1 + q) % G] + i, x);   // next peer first: spread links
+#pragma unroll
+    for (int j = 0; j < N; ++j) bad |= !isfinite(x[j]);
+}
+
+template <int WIRE, int G>
+__global__ void __launch_bounds__(kPeerThreads) avg_publish_kernel(const PeerArgs pa) {
+    bool bad = false;
+    const int64_t n = pa.a.n;
+    const int64_t nch = n / kPV;
+    const int64_t stride = int64_t(gridDim.x) * kPeerThreads;
+    for (int64_t c = int64_t(blockIdx.x) * kPeerThreads + threadIdx.x; c < nch; c += stride)
+        avg_publish_body<WIRE, G, kPV>(pa, c * kPV, bad);
+    if (blockIdx.x == gridDim.x - 1) {
+        const int64_t i = nch * kPV + threadIdx.x;
+        if (i < n) avg_publish_body<WIRE, G, 1>(pa, i, bad);
+    }
+    if (pa.a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (threadIdx.x & 31) == 0) atomicOr(pa.a.flag, 1u);
+    }
+    end_barrier(pa, G);
+}
+
+// The same tail with the NVLink stores done by the bulk-copy engine: each 2048-parameter tile is
+// averaged in registers (8 per thread), written to one of two shared-memory output buffers, and
+// one thread issues a bulk store of the buffer to every node peer (cp.async.bulk shared -> peer
+// global).  Bulk stores reached 0.84 of the link in the probe against 0.79 for register stores.
+constexpr int kAvgOut = 2;
+
+template <int WIRE, int G>
+__global__ void __launch_bounds__(kPeerThreads) avg_publish_tma_kernel(const PeerArgs pa) {
+    __shared__ __align__(128) float ob[kAvgOut][kPT];
+    const KernelArgs& a = pa.a;
+    const int tid = threadIdx.x;
+    const int64_t ntiles = a.n / kPT;
+    bool bad = false;
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int o = k % kAvgOut;
+        const int64_t e0 = t * kPT;
+        float x[kPV];
+#pragma unroll
+        for (int j = 0; j < kPV; ++j) x[j] = 0.f;
+#pragma unroll 4
+        for (int p = 0; p < a.P; ++p) {
+            float sv[kPV];
+            Wire<WIRE>::template load<kPV>(a.slot, p * a.slot_stride + e0 + tid * kPV, sv);
+#pragma unroll
+            for (int j = 0; j < kPV; ++j) x[j] += sv[j];                     // ascending node order (R18)
+        }
+#pragma unroll
+        for (int j = 0; j < kPV; ++j) {
+            x[j] = x[j] / a.den;
+            bad |= !isfinite(x[j]);
+        }
+        if (tid == 0 && k >= kAvgOut) bulk_wait_read<kAvgOut - 1>();        // buffer o has been read
+        __syncthreads();
+        Wire<DASO_WIRE_FP32>::template store_smem<kPV>(ob[o], tid * kPV, x);
+        fence_async_smem();                                                  // generic writes -> bulk stores
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int q = 0; q < G; ++q) bulk_s2g(pa.xp[(pa.me + 1 + q) % G] + e0, ob[o], kPT * 4);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+    if (blockIdx.x == gridDim.x - 1)                                         // ragged tail (< one tile)
+        for (int64_t e = ntiles * kPT + tid; e < a.n; e += kPeerThreads) avg_publish_body<WIRE, G, 1>(pa, e, bad);
+    if (a.flag != nullptr) {
+        const unsigned any = __ballot_sync(0xffffffffu, bad);
+        if (any != 0u && (tid & 31) == 0) atomicOr(a.flag, 1u);
+    }
+    if (tid == 0) fence_proxy_async_global();
+    end_barrier(pa, G);
+}
+
+// DASO_AVG_PUBLISH=ldg|tma (default tma); the TMA form needs 16-byte aligned peer shards
+int avg_publish_path() {
+    const char* e = getenv("DASO_AVG_PUBLISH");
+    return (e && strcmp(e, "ldg") == 0) ? 0 : 1;
+}
+
+template <int WIRE, int G>
+int launch_avg_publish_t(const PeerArgs& pa, cudaStream_t s, int sms) {
+    uintptr_t al = reinterpret_cast<uintptr_t>(pa.a.slot);
+    for (int q = 0; q < G; ++q) al |= reinterpret_cast<uintptr_t>(pa.xp[q]);
+    if (avg_publish_path() == 1 && (al & 15u) == 0 && pa.a.n >= kPT) {
+        // two CTAs per SM on SMs - 16 (the side-stream exchange keeps free SMs, as for the node tier)
+        const int grid = 2 * std::max(1, sms - 16);
+        avg_publish_tma_kernel<WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), 0, s>>>(pa);
+        return int(cudaGetLastError());
+    }
+    const int64_t nch = pa.a.n / kPV;
+    int64_t blocks = (nch + kPeerThreads - 1) / kPeerThreads;
+    blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, int64_t(sms) * peer_blocks_per_sm()));
+    avg_publish_kernel<WIRE, G><<<dim3(unsigned(blocks)), dim3(kPeerThreads), 0, s>>>(pa);
+    return int(cudaGetLastError());
+}
+
+template <int WIRE>
+int dispatch_avg_publish(const PeerArgs& pa, cudaStream_t s, int sms) {
+    switch (pa.G) {
+        case 1: return launch_avg_publish_t<WIRE, 1>(pa, s, sms);
+        case 2: return launch_avg_publish_t<WIRE, 2>(pa, s, sms);
+        case 3: return launch_avg_publish_t<WIRE, 3>(pa, s, sms);
+        case 4: return launch_avg_publish_t<WIRE, 4>(pa, s, sms);
+        case 5: return launch_avg_publish_t<WIRE, 5>(pa, s, sms);
+        case 6: return launch_avg_publish_t<WIRE, 6>(pa, s, sms);
+        case 7: return launch_avg_publish_t<WIRE, 7>(pa, s, sms);
+        case 8: return launch_avg_publish_t<WIRE, 8>(pa, s, sms);
+        default: return int(cudaErrorInvalidValue);
+    }
 }
 
 // Peer data path under daso_kernel_impl(2) "auto" (DASO_PEER=ws|tma|ldg).
