@@ -208,7 +208,15 @@ daso_status daso_global_merge(daso_ctx* c, void* stream);
  * broadcast after a merge, side-stream group all-gather for a send, and — blocking
  * — the average kernel and broadcast.  Sharded / fused modes run the same batch
  * element-sharded over the node; fused puts the whole node tier
- * in one kernel.  `lr` is this batch's learning rate; `plateau` as in daso_sched_next.
+ * in one kernel.  Blocking batches of the fused mode (Fig. 3 / Fig. 4): the node-tier
+ * kernel only packs (no parameter stores), the group exchange runs, then one kernel averages
+ * the P rows of the shard and stores the result into every node peer's x, ending with the
+ * node barrier.  With the copy-engine transport the local pack kernel of a blocking batch
+ * (G = 1, sharded mode) stores the packed row straight into every group member's slot
+ * (environment DASO_BLOCKING_PUSH: 0 never, 1 local pack kernels (default), 2 also the
+ * fused node-tier kernel; DASO_AVG_PUBLISH=ldg|tma selects the tail's store path; all
+ * choices give bit-identical results).
+ * `lr` is this batch's learning rate; `plateau` as in daso_sched_next.
  * Errors: DASO_ERR_PROTOCOL (not bound; schedule/flight-state mismatch), asynchronous
  * DASO_ERR_CUDA / DASO_ERR_NCCL from earlier work. */
 daso_status daso_step(daso_ctx* c, float lr, int plateau, void* stream, daso_record* out);

@@ -628,31 +628,41 @@ __global__ void __launch_bounds__(kPeerThreads) avg_publish_kernel(const PeerArg
 }
 
 // The same tail with the NVLink stores done by the bulk-copy engine: each 2048-parameter tile is
-// averaged in registers (8 per thread), written to one of two shared-memory output buffers, and
+// averaged in registers (8 per thread), written to one of kAvgOut shared-memory output buffers, and
 // one thread issues a bulk store of the buffer to every node peer (cp.async.bulk shared -> peer
 // global).  Bulk stores reached 0.84 of the link in the probe against 0.79 for register stores.
-constexpr int kAvgOut = 2;
+// P (<= 4) is a template parameter so the next tile's P row loads are issued into registers before
+// the current tile is stored (a first version without the prefetch was load-latency bound: 64 us
+// for a 2x2 shard in the one-GPU virtual cluster at 18 % DRAM throughput, profiles/r02/one_s).
+constexpr int kAvgOut = 4;
 
-template <int WIRE, int G>
+template <int WIRE, int G, int PT>
 __global__ void __launch_bounds__(kPeerThreads) avg_publish_tma_kernel(const PeerArgs pa) {
     __shared__ __align__(128) float ob[kAvgOut][kPT];
     const KernelArgs& a = pa.a;
     const int tid = threadIdx.x;
     const int64_t ntiles = a.n / kPT;
     bool bad = false;
-    int k = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    float cur[PT][kPV];
+    auto load_tile = [&](int64_t t, float (&dst)[PT][kPV]) {
+#pragma unroll
+        for (int p = 0; p < PT; ++p)
+            Wire<WIRE>::template load<kPV>(a.slot, p * a.slot_stride + t * kPT + tid * kPV, dst[p]);
+    };
+    int64_t t = blockIdx.x;
+    if (t < ntiles) load_tile(t, cur);
+    for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
         const int o = k % kAvgOut;
         const int64_t e0 = t * kPT;
+        float nxt[PT][kPV];
+        if (t + gridDim.x < ntiles) load_tile(t + gridDim.x, nxt);           // next tile's rows in flight
         float x[kPV];
 #pragma unroll
         for (int j = 0; j < kPV; ++j) x[j] = 0.f;
-#pragma unroll 4
-        for (int p = 0; p < a.P; ++p) {
-            float sv[kPV];
-            Wire<WIRE>::template load<kPV>(a.slot, p * a.slot_stride + e0 + tid * kPV, sv);
 #pragma unroll
-            for (int j = 0; j < kPV; ++j) x[j] += sv[j];                     // ascending node order (R18)
+        for (int p = 0; p < PT; ++p) {
+#pragma unroll
+            for (int j = 0; j < kPV; ++j) x[j] += cur[p][j];                 // ascending node order (R18)
         }
 #pragma unroll
         for (int j = 0; j < kPV; ++j) {
@@ -668,6 +678,11 @@ __global__ void __launch_bounds__(kPeerThreads) avg_publish_tma_kernel(const Pee
 #pragma unroll
             for (int q = 0; q < G; ++q) bulk_s2g(pa.xp[(pa.me + 1 + q) % G] + e0, ob[o], kPT * 4);
             bulk_commit();
+        }
+#pragma unroll
+        for (int p = 0; p < PT; ++p) {
+#pragma unroll
+            for (int j = 0; j < kPV; ++j) cur[p][j] = nxt[p][j];
         }
     }
     if (tid == 0) bulk_wait_all();
@@ -691,10 +706,15 @@ template <int WIRE, int G>
 int launch_avg_publish_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     uintptr_t al = reinterpret_cast<uintptr_t>(pa.a.slot);
     for (int q = 0; q < G; ++q) al |= reinterpret_cast<uintptr_t>(pa.xp[q]);
-    if (avg_publish_path() == 1 && (al & 15u) == 0 && pa.a.n >= kPT) {
+    if (avg_publish_path() == 1 && (al & 15u) == 0 && pa.a.n >= kPT && pa.a.P >= 1 && pa.a.P <= 4) {
         // two CTAs per SM on SMs - 16 (the side-stream exchange keeps free SMs, as for the node tier)
-        const int grid = 2 * std::max(1, sms - 16);
-        avg_publish_tma_kernel<WIRE, G><<<dim3(unsigned(grid)), dim3(kPeerThreads), 0, s>>>(pa);
+        const dim3 grid(unsigned(2 * std::max(1, sms - 16)));
+        switch (pa.a.P) {
+            case 1: avg_publish_tma_kernel<WIRE, G, 1><<<grid, kPeerThreads, 0, s>>>(pa); break;
+            case 2: avg_publish_tma_kernel<WIRE, G, 2><<<grid, kPeerThreads, 0, s>>>(pa); break;
+            case 3: avg_publish_tma_kernel<WIRE, G, 3><<<grid, kPeerThreads, 0, s>>>(pa); break;
+            default: avg_publish_tma_kernel<WIRE, G, 4><<<grid, kPeerThreads, 0, s>>>(pa); break;
+        }
         return int(cudaGetLastError());
     }
     const int64_t nch = pa.a.n / kPV;
