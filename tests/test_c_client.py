@@ -31,3 +31,30 @@ def test_plain_c_client(tmp_path):
              r.merge_group, r.pending, r.due) for r in recs]
     assert [plateau_arg(k, flags, 8) for k in (16, 24)] == [1, 1]
     assert got == want
+
+
+@pytest.mark.skipif(shutil.which("gcc") is None, reason="needs gcc")
+def test_binding_structs_match_the_header_layout(tmp_path):
+    """The ctypes mirrors of the header's structs (argument marshalling at the boundary) have the C
+    compiler's size and field offsets, so no field is read from the wrong place (e.g. daso_trace's
+    kernel_nvl_bytes appended in round 2)."""
+    structs = {"daso_sched_config": L.SchedConfig, "daso_record": L.Record, "daso_config": L.Config,
+               "daso_trace": L.Trace}
+    src = ["#include <stddef.h>", "#include <stdio.h>", '#include "daso.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        src.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            src.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src += ["  return 0;", "}"]
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src) + "\n")
+    exe = str(tmp_path / "layout")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(c), "-o", exe],
+                   check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(line.split()[:2]): int(line.split()[2]) for line in out if line}
+    import ctypes
+    for cname, cls in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
