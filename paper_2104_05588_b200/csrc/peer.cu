@@ -387,22 +387,36 @@ int launch_peer_tma_t(const PeerArgs& pa, cudaStream_t s, int sms) {
 // The driver refills a stage as soon as its tile is computed and issues the stores of every
 // output buffer as soon as it is written, so NVLink reads, NVLink stores and compute of
 // different tiles overlap continuously; no thread ever waits for the whole CTA.
-constexpr int kWsCompute = 256, kWsThreads = kWsCompute + 32, kWsOut = 2;
+constexpr int kWsCompute = 256, kWsThreads = kWsCompute + 32, kWsMaxOut = 4;
+
+// cp.async.bulk.wait_group.read takes an immediate: dispatch the runtime count (1..kWsMaxOut-1)
+__device__ __forceinline__ void bulk_wait_read_upto(int n) {
+    if (n <= 1) bulk_wait_read<1>();
+    else if (n == 2) bulk_wait_read<2>();
+    else bulk_wait_read<3>();
+}
+
+// Output buffers of the warp-specialised kernel (DASO_PEER_OUT = 2..4, default 2): how many tiles'
+// bulk stores may still be reading their shared-memory buffers while the compute warps fill the next.
+int peer_ws_out() {   // read per launch, so a test can compare the settings in one process
+    const char* e = getenv("DASO_PEER_OUT");
+    return e ? std::max(2, std::min(kWsMaxOut, atoi(e))) : 2;
+}
 
 template <int OPS, int WIRE, int G>
-__global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs pa, int NS) {
+__global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs pa, int NS, int NO) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
     const KernelArgs& a = pa.a;
     const PeerTmaLayout L = peer_tma_layout(OPS, G, a.P, wb);
     unsigned char* outs = smem + size_t(NS) * L.in_bytes;
-    uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(kWsOut) * L.out_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(outs + size_t(NO) * L.out_bytes);
     uint64_t* ofull = full + NS;
-    uint64_t* oempty = ofull + kWsOut;
+    uint64_t* oempty = ofull + NO;
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-        for (int o = 0; o < kWsOut; ++o) {
+        for (int o = 0; o < NO; ++o) {
             mbar_init(&ofull[o], kWsCompute / 32);
             mbar_init(&oempty[o], 1);
         }
@@ -460,8 +474,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
         if (ok)
             for (int64_t k = 0; k < my && k < NS; ++k) issue_remote(k);
         for (int64_t k = 0; k < my && ok; ++k) {
-            const int o = int(k % kWsOut);
-            if (!mbar_wait(&ofull[o], uint32_t((k / kWsOut) & 1), pa.err)) break;
+            const int o = int(k % NO);
+            if (!mbar_wait(&ofull[o], uint32_t((k / NO) & 1), pa.err)) break;
             if (k + NS < my) issue_load(k + NS);                // stage k % NS consumed: refill it
             unsigned char* ob = outs + size_t(o) * L.out_bytes;
             const int64_t e0 = tile0(k);
@@ -483,15 +497,15 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
                 }
             }
             bulk_commit();
-            if (k >= 1) {                                       // the previous tile's buffer has been read
-                bulk_wait_read<1>();
-                mbar_arrive(&oempty[(k - 1) % kWsOut]);
+            if (k >= NO - 1) {                                  // up to NO-1 tiles' stores may still read
+                bulk_wait_read_upto(NO - 1);                    // their buffers; tile k-(NO-1)'s has been read
+                mbar_arrive(&oempty[(k - (NO - 1)) % NO]);
             }
         }
         bulk_wait_all();
     } else if (tid < kWsCompute) {   // ---- compute warps
         for (int64_t k = 0; k < my; ++k) {
-            const int s = int(k % NS), o = int(k % kWsOut);
+            const int s = int(k % NS), o = int(k % NO);
             unsigned char* st = smem + size_t(s) * L.in_bytes;
             unsigned char* ob = outs + size_t(o) * L.out_bytes;
             if (!mbar_wait(&full[s], uint32_t((k / NS) & 1), pa.err)) break;
@@ -526,7 +540,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) peer_ws_kernel(const PeerArgs p
 #pragma unroll
                 for (int j = 0; j < 8; ++j) x[j] = x[j] + acc[j] / a.den;
             }
-            if (k >= kWsOut && !mbar_wait(&oempty[o], uint32_t(((k / kWsOut) - 1) & 1), pa.err)) break;
+            if (k >= NO && !mbar_wait(&oempty[o], uint32_t(((k / NO) - 1) & 1), pa.err)) break;
             if constexpr ((OPS & OP_NOX) == 0) Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ox, i, x);
             Wire<DASO_WIRE_FP32>::template store_smem<8>(ob + L.ov, i, v);
             if constexpr ((OPS & OP_PACK) != 0) Wire<WIRE>::template store_smem<8>(ob + L.opack, i, x);
@@ -563,10 +577,11 @@ template <int OPS, int WIRE, int G>
 int launch_peer_ws_t(const PeerArgs& pa, cudaStream_t s, int sms) {
     constexpr int wb = WIRE == DASO_WIRE_BF16 ? 2 : 4;
     const PeerTmaLayout L = peer_tma_layout(OPS, G, pa.a.P, wb);
-    const int budget = 210 * 1024 - kWsOut * int(L.out_bytes);
+    const int NO = peer_ws_out();
+    const int budget = 210 * 1024 - NO * int(L.out_bytes);
     const int NS = int(std::min<int64_t>(8, (budget - 128) / L.in_bytes));
     if (NS < 2) return launch_peer_t<OPS, WIRE, G>(pa, s, sms);
-    const size_t smem = size_t(NS) * L.in_bytes + size_t(kWsOut) * L.out_bytes + 8 * size_t(NS + 2 * kWsOut);
+    const size_t smem = size_t(NS) * L.in_bytes + size_t(NO) * L.out_bytes + 8 * size_t(NS + 2 * NO);
     static size_t attr = 0;
     if (smem > attr) {
         const cudaError_t e = cudaFuncSetAttribute(peer_ws_kernel<OPS, WIRE, G>,
@@ -575,7 +590,7 @@ int launch_peer_ws_t(const PeerArgs& pa, cudaStream_t s, int sms) {
         attr = smem;
     }
     const int grid = peer_tma_ctas() > 0 ? std::min(peer_tma_ctas(), sms) : std::max(1, sms - 16);
-    peer_ws_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kWsThreads), smem, s>>>(pa, NS);
+    peer_ws_kernel<OPS, WIRE, G><<<dim3(unsigned(grid)), dim3(kWsThreads), smem, s>>>(pa, NS, NO);
     return int(cudaGetLastError());
 }
 

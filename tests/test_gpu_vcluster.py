@@ -265,3 +265,38 @@ def test_vcluster_avg_publish_paths_bit_identical(P, G, monkeypatch):
     for r in range(P * G):
         for k in range(len(a[r])):
             np.testing.assert_array_equal(a[r][k].view(np.uint32), b[r][k].view(np.uint32))
+
+
+def _run_vc_microbench(P, G, n, steps, B=4, S=1):
+    vc = daso.VCluster(P * G, G, B, S, n, total_epochs=1, steps_per_epoch=B << 20, mode="fused")
+    try:
+        x0 = torch.from_numpy(synthetic.microbench_x0(n)).cuda()
+        for r in range(P * G):
+            vc.x(r)[:n] = x0
+        out = []
+        for k in range(steps):
+            for r in range(P * G):
+                vc.g(r)[:n] = torch.from_numpy(synthetic.microbench_grad(n, r, k)).cuda()
+            vc.step(0.1)
+            out.append([vc.x(r)[:n].cpu().numpy().view(np.uint32).copy() for r in range(P * G)])
+        for r in range(P * G):
+            assert vc.rank(r).check_finite()
+        return out
+    finally:
+        vc.destroy()
+
+
+@pytest.mark.parametrize("P,G", [(1, 2), (2, 2)])
+def test_vcluster_ws_output_buffers_bit_identical(P, G, monkeypatch):
+    """The warp-specialised node-tier kernel with 2 (default) and 4 shared-memory output buffers
+    (DASO_PEER_OUT) on shards of 1.5M parameters — several tiles per persistent CTA, so the buffer
+    rotation and the release of buffers whose bulk stores have read them are exercised — gives
+    bitwise identical parameters for every rank and step, including a merge and a send (B = 4, S = 1)."""
+    n = 3_000_000
+    monkeypatch.setenv("DASO_PEER_OUT", "2")
+    a = _run_vc_microbench(P, G, n, 3)
+    monkeypatch.setenv("DASO_PEER_OUT", "4")
+    b = _run_vc_microbench(P, G, n, 3)
+    for k in range(3):
+        for r in range(P * G):
+            np.testing.assert_array_equal(a[k][r], b[k][r])
