@@ -71,6 +71,8 @@ def parse():
                     help="fwd/bwd stand-in per batch inside the hidden-fraction cycles (P > 1); config 3's "
                          "real fwd/bwd (~55 ms at 256/GPU) hides the exchange trivially but drowns it in noise")
     ap.add_argument("--cycles", type=int, default=30, help="B-cycles per leg of the hidden-fraction measurement")
+    ap.add_argument("--gemm-cycles", type=int, default=120,
+                    help="B-cycles per leg with the GEMM stand-in (its cycle-to-cycle jitter is ~10x the exchange)")
     ap.add_argument("--overlap-compute", choices=["gemm", "sleep", "both"], default="both",
                     help="fwd/bwd stand-in of the hidden-fraction cycles: bf16 GEMMs (SM/HBM contention, jittery), "
                          "a deterministic device sleep (precise), or both")
@@ -411,7 +413,7 @@ def make_sleep(ms: float):
     return lambda: torch.cuda._sleep(cycles)
 
 
-def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t_ag):
+def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t_ag, cycles=None):
     """SURVEY §8(d) hidden fraction: hidden = 1 - (T_with - T_without) / T_AG,alone, per B-cycle.
     One cycle = B batches of [fwd/bwd stand-in (bf16 GEMMs) ; gradient refresh ; daso_step], timed by
     CUDA events on the compute stream from the cycle's first batch to the end of its last.  In
@@ -421,9 +423,12 @@ def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t
     same cycles with the group all-gather suppressed (daso_set_exchange(0)).  The two legs
     alternate block by block (a block is 1 cycle, or 2 when S = B so that the timed cycle's merge
     waits for an exchange of its own leg) to cancel clock and power drift; T_AG,alone is measured
-    before the bench's first step (daso_exchange_alone)."""
+    before the bench's first step (daso_exchange_alone).  The exposed time is the median of the
+    paired differences (cycle 2i with the exchange minus cycle 2i+1 without), which cancels drift
+    slower than two cycles; the difference of the two legs' medians is reported beside it."""
     import torch
     block = 1 if a.S < a.B else 2
+    cycles = cycles or a.cycles
 
     def batch():
         compute()
@@ -433,7 +438,7 @@ def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t
     while ctx.query()["batch_in_cycle"] != a.B - 1:   # align: the next batch starts a cycle
         batch()
     legs = {True: [], False: []}
-    for c in range(2 * a.cycles):
+    for c in range(2 * cycles):
         enabled = c % 2 == 0
         ctx.set_exchange(enabled)
         for _ in range(block - 1):
@@ -451,13 +456,14 @@ def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t
     t_without = [e0.elapsed_time(e1) for e0, e1 in legs[False]]
     w_med = max_over_ranks(statistics.median(t_with), world)
     wo_med = max_over_ranks(statistics.median(t_without), world)
-    exposed = w_med - wo_med
+    exposed = max_over_ranks(statistics.median([w - wo for w, wo in zip(t_with, t_without)]), world)
     hidden = 1.0 - max(0.0, exposed) / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
     spread = max_over_ranks(pct(t_without, 0.9) - pct(t_without, 0.1), world)
-    return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); medians over "
-                   "alternating cycles, max over ranks; T_AG,alone before the first step",
-            "cycles_per_leg": a.cycles, "compute_ms_per_batch": a.overlap_compute_ms,
+    return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); exposed = median of "
+                   "the paired differences of alternating cycles, max over ranks; T_AG,alone before the first step",
+            "cycles_per_leg": cycles, "compute_ms_per_batch": a.overlap_compute_ms,
             "T_cycle_with_ms": w_med, "T_cycle_without_ms": wo_med, "exposed_ms": exposed,
+            "exposed_ms_from_leg_medians": w_med - wo_med,
             "T_cycle_without_p10_p90_spread_ms": spread,
             "T_AG_alone_ms": t_ag, "exchanges_per_cycle": n_exch_per_cycle, "hidden_fraction": hidden}
 
@@ -597,7 +603,8 @@ def run_ours(a):
                                               t_ag)
         if a.overlap_compute in ("gemm", "both"):
             overlap["gemm"] = overlap_cycles(ctx, a, g, g_src, stream, world,
-                                             make_compute_small(a.overlap_compute_ms, dev), nx, t_ag)
+                                             make_compute_small(a.overlap_compute_ms, dev), nx, t_ag,
+                                             cycles=max(a.cycles, a.gemm_cycles))
 
     # ---- e2e through the C ABI with host buffers (daso_step_host) -------------------------------
     e2e = None
