@@ -16,8 +16,14 @@ KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "lts__t_sector_hit_rate.pct"]
 
 
+OURS = ("fused_kernel", "average_kernel", "tma_kernel", "peer_kernel", "peer_tma_kernel", "peer_ws_kernel",
+        "avg_publish_kernel", "avg_publish_tma_kernel", "copy_tensors_kernel", "checksum_kernel", "fill_u64_kernel")
+
+
 def short(name):
-    if "unnamed" in name or "daso" in name:
+    if "at::cuda" in name or "spin_kernel" in name:
+        return "torch: " + name.split("(")[0][-60:]
+    if "daso" in name or any(k + "<" in name or k + "(" in name for k in OURS):
         base = name.split("(daso::")[0] if "(daso::" in name else name.split("(")[0]
         return "libdaso::" + base.split("::")[-1]
     if "nccl" in name.lower():
