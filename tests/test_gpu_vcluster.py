@@ -300,3 +300,61 @@ def test_vcluster_ws_output_buffers_bit_identical(P, G, monkeypatch):
     for k in range(3):
         for r in range(P * G):
             np.testing.assert_array_equal(a[k][r], b[k][r])
+
+
+@pytest.mark.parametrize("P,G", [(2, 2), (4, 1)])
+def test_vcluster_full_size_blocking_sampled(P, G, monkeypatch):
+    """Blocking syncs (B = 1, S = 0: every batch Fig. 3 average + Fig. 4 re-publish) at config 2's
+    full size through the copy-engine exchange: at 2x2 the node-tier kernel without its parameter
+    stores and the bulk-store average / re-publish kernel on 12.8M-parameter shards (many tiles per
+    CTA: the output-buffer rotation and the next-tile prefetch run), at 4x1 the local K2 pushing
+    the packed row into the group members' slots and the P-specialised K4.  Sampled parameters of
+    every rank against the oracle (elementwise given the gradients), node replicas bitwise equal,
+    and the register-store tail bitwise equal to the bulk-store tail."""
+    import mp_micro
+    N, steps = mp_micro.N, 3
+    idx = mp_micro.sample_indices()
+    torch.cuda.set_device(0)
+    tidx = torch.from_numpy(idx).cuda()
+
+    def run():
+        vc = daso.VCluster(P * G, G, 1, 0, N, total_epochs=1, steps_per_epoch=1 << 20, momentum=0.9,
+                           weight_decay=1e-4, wire="bf16", mode="fused", exchange="ce")
+        try:
+            x0 = torch.from_numpy(synthetic.microbench_x0(N)).cuda()
+            for r in range(P * G):
+                vc.x(r)[:N] = x0
+            trace = [[] for _ in range(P * G)]
+            for k in range(steps):
+                for r in range(P * G):
+                    vc.g(r)[:N] = torch.from_numpy(synthetic.microbench_grad(N, r, k)).cuda()
+                vc.step(0.1)
+                for r in range(P * G):
+                    trace[r].append(vc.x(r)[tidx].cpu().numpy())
+            for r in range(P * G):
+                assert vc.rank(r).check_finite()
+            return trace
+        finally:
+            vc.destroy()
+
+    monkeypatch.setenv("DASO_AVG_PUBLISH", "tma")
+    trace = run()
+    grads = {(r, k): synthetic.microbench_grad(N, r, k)[idx] for r in range(P * G) for k in range(steps)}
+    cfg = SchedConfig(B_init=1, S_init=0, total_epochs=1, steps_per_epoch=1 << 20)
+    ref = daso_sim.simulate(P, G, cfg, steps, synthetic.microbench_x0(N)[idx], lambda r, k, w: grads[(r, k)],
+                            0.1, 0.9, 1e-4, wire="bf16", trace=True)
+    for r in range(P * G):
+        for k in range(steps):
+            xo = ref["trace"][k][r]
+            rms = np.sqrt(np.mean(xo ** 2))
+            assert np.all(np.abs(trace[r][k] - xo) <= 1e-2 * (np.abs(xo) + rms)), (r, k)
+    for j in range(P):
+        for l in range(1, G):
+            for k in range(steps):
+                np.testing.assert_array_equal(trace[j * G + l][k], trace[j * G][k])
+    if G > 1:
+        monkeypatch.setenv("DASO_AVG_PUBLISH", "ldg")
+        other = run()
+        for r in range(P * G):
+            for k in range(steps):
+                np.testing.assert_array_equal(other[r][k].view(np.uint32), trace[r][k].view(np.uint32))
