@@ -4,10 +4,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
 
-One step = one DASO batch of the whole hot path through the C ABI (daso_step):
-node all-reduce of the gradient bucket, the fused update (+ Eq. (1) merge, + bf16
-pack) kernel, node broadcast after merges, and every B-th batch the non-blocking
-bf16 group all-gather on the side stream, driven by the B/S schedule.
+One step = one DASO batch of the whole hot path through the C ABI (daso_step), driven
+by the B/S schedule.  In the default fused mode: one node-tier kernel per GPU reduces the
+node's gradient shards over NVLink, applies the update (+ Eq. (1) merge when due, + bf16
+pack when sending) and stores the new parameter shard into every node peer; every B-th
+batch the packed shard goes to the group members by copy-engine pushes on the library's
+side streams (non-blocking, merged S batches later); blocking batches (S = 0) end with the
+average / re-publish kernel.  (faithful mode: NCCL node all-reduce, fused update kernel,
+node broadcast after merges, group all-gather.)
 Workload: n = 25,557,032 fp32 parameters (ResNet-50-sized), synthetic seeded
 gradients, B = 4, S = 1, topology P x G virtual nodes: N=1 -> 1x1,
 2 -> 2x1, 4 -> 2x2, 8 -> 2x4.
