@@ -13,6 +13,9 @@
 //   push_rs  : write-only node tier, phase A: every GPU stores its g tile q into owner q's
 //              receive buffer (remote 128-bit stores), phase B = tma_w; reported per phase
 //   ce_bidi  : copy engines, every GPU copies (G-1)/G 4n to its peers (cudaMemcpyPeerAsync)
+//   tma_r+ce_w: the node tier's two halves on different engines at once — SM bulk reads of the
+//              peers' g tiles (tma_r) while the copy engines push (G-1)/G 4n to the peers' x
+//   ce_rw    : both halves on copy engines — pulls of the peers' g shards + pushes to their x
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/nvk tools/nvlink_kernels.cu
 //   /tmp/nvk [n_params] [ctas (0 = SMs-16)] [stages (0 = auto)] [tile floats (2048)]
@@ -234,6 +237,39 @@ int main(int argc, char** argv) {
     for (int bpsm : {2, 4, 8})
         run((std::string("push_rs_phaseA_bpsm") + std::to_string(bpsm)).c_str(), one,
             [&](int d) { push_kernel<<<sms * bpsm, kThr, 0, st[d]>>>(args(d)); });
+    std::vector<cudaStream_t> st2(G);
+    std::vector<cudaEvent_t> fork(G), join(G);
+    for (int d = 0; d < G; ++d) {
+        CK(cudaSetDevice(d));
+        CK(cudaStreamCreateWithFlags(&st2[d], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&fork[d], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&join[d], cudaEventDisableTiming));
+    }
+    auto ce_push = [&](int d, cudaStream_t s) {
+        for (int k = 1; k < G; ++k) {
+            const int q = (d + k) % G;
+            CK(cudaMemcpyPeerAsync(x[q] + size_t(d) * n, q, r[d] + size_t(d) * n, d, size_t(n) * 4, s));
+        }
+    };
+    run("tma_r+ce_w", 2 * one, [&](int d) {
+        CK(cudaEventRecord(fork[d], st[d]));
+        CK(cudaStreamWaitEvent(st2[d], fork[d], 0));
+        tma_kernel<true, false><<<ctas, kThr, smem, st[d]>>>(args(d));
+        ce_push(d, st2[d]);
+        CK(cudaEventRecord(join[d], st2[d]));
+        CK(cudaStreamWaitEvent(st[d], join[d], 0));
+    });
+    run("ce_rw", 2 * one, [&](int d) {
+        CK(cudaEventRecord(fork[d], st[d]));
+        CK(cudaStreamWaitEvent(st2[d], fork[d], 0));
+        for (int k = 1; k < G; ++k) {   // pulls: peer q's g at this GPU's shard -> local receive buffer
+            const int q = (d + k) % G;
+            CK(cudaMemcpyPeerAsync(r[d] + size_t(q) * n, d, g[q] + size_t(d) * n, q, size_t(n) * 4, st[d]));
+        }
+        ce_push(d, st2[d]);
+        CK(cudaEventRecord(join[d], st2[d]));
+        CK(cudaStreamWaitEvent(st[d], join[d], 0));
+    });
     run("ce_bidi", one, [&](int d) {
         for (int q = 0; q < G; ++q)
             if (q != d) CK(cudaMemcpyPeerAsync(x[q] + size_t(d) * n, q, g[d] + size_t(q) * n, d, size_t(n) * 4, st[d]));
