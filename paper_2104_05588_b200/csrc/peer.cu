@@ -14,6 +14,9 @@
 //      system-scope fence and waits for all peers, so when the kernel completes every
 //      GPU of the node holds the full new x and no peer still reads this rank's g.
 // Node replicas stay bitwise identical; the arithmetic per element is K1/K3's.
+// Blocking batches (Fig. 3) run the kernel as OP_NOX (pack only: no x stores, no end
+// barrier) and finish with avg_publish_[tma_]kernel: the group average of the shard stored into
+// every peer's x, then the end barrier (Fig. 4 re-publish).
 // Each rank is its own GPU (one process per GPU), so the spin-waits never wait on a
 // kernel of the same GPU; the grid leaves room on every SM for the side-stream NCCL
 // exchange kernels to run concurrently.
