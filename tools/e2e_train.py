@@ -120,6 +120,9 @@ def main():
                     help="instead of timing: train this many epochs with the full loop of P:97-99/P:162/P:172 — "
                          "epoch-mean loss -> plateau detector -> LR decay and DASO B/S halving (N4)")
     ap.add_argument("--steps-per-epoch", type=int, default=8)
+    ap.add_argument("--timed-phase", choices=["cycling", "warmup"], default="cycling",
+                    help="DASO phase of the timed steps (P:97): cycling (non-blocking exchange every B batches) "
+                         "or warm-up (a blocking sync every batch)")
     ap.add_argument("--patience", type=int, default=2)
     ap.add_argument("--threshold", type=float, default=0.01)
     ap.add_argument("--lr-warmup-epochs", type=int, default=1)
@@ -186,9 +189,11 @@ def main():
             ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
                                  total_epochs=max(a.train_epochs, 2), steps_per_epoch=a.steps_per_epoch, mode=a.mode,
                                  exchange=a.exchange)
-        else:
-            ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid, warmup_epochs=1, cooldown_epochs=1,
-                                 total_epochs=1000, steps_per_epoch=10 * 4, mode=a.mode, exchange=a.exchange)
+        else:   # the timed steps all fall in the first epoch: warm-up (blocking) or, without one, cycling
+            ctx = daso.daso_init(world, G, B, S, rank=rank, uid=uid,
+                                 warmup_epochs=1 if a.timed_phase == "warmup" else 0, cooldown_epochs=1,
+                                 total_epochs=1000, steps_per_epoch=4 * (a.warmup + a.steps + 4), mode=a.mode,
+                                 exchange=a.exchange)
         if a.mode == "fused" and "expandable_segments:True" in os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""):
             # cuMem-backed torch memory cannot be exported by CUDA IPC: let the library own the buckets
             flat = daso.FlatParams(model.parameters(), gpus_per_node=G, ctx=ctx)
@@ -249,6 +254,7 @@ def main():
         tr = ctx.trace_read(reset=True)
         sync_ms = (tr["kernel_ms"] + tr["local_ms"] + tr["node_ms"] + tr["wait_ms"]) / a.steps
         out.update({"topology": f"{ctx.P}x{ctx.G}", "mode": a.mode, "exchange": a.exchange, "overlap": a.overlap,
+                    "timed_phase": a.timed_phase if a.impl == "daso" else "sync every batch",
                     "sync_path_ms_per_step": sync_ms,
                     "sync_share": sync_ms / (ms / a.steps), "finite": ctx.check_finite()})
         ctx.finalize()
