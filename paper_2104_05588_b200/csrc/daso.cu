@@ -312,11 +312,14 @@ daso_status push_exchange(daso_ctx* c, cudaStream_t s) {
 // after it, raise the arrival flag e in every member's xs (cuStreamWriteValue64 orders it after the
 // kernel's stores).  Not in a batch that also merges: there this rank's acknowledgement of e-1
 // follows the kernel, and the members wait for it before their own kernel pushes.
-// Where: by default only from the local pack kernel (G = 1, or the sharded mode), whose links are
+// Where: by default from the local pack kernel (G = 1, or the sharded mode), whose links are
 // otherwise idle — 4x1 blocking batch 0.468 -> 0.332 ms.  Inside the fused node-tier kernel (G > 1)
-// the push shares the links with the peer gradient reads and measured slower than the copy-engine
-// pushes after it (2x2: 0.309 vs 0.292 ms, profiles/r02/multi4_k).  DASO_BLOCKING_PUSH: 0 never,
-// 1 local pack kernels (default), 2 also the fused node-tier kernel.
+// the push shares the links with the peer gradient reads; with a group of two it measured slower
+// than the copy-engine push after the kernel (2x2: 0.309 vs 0.292 ms, profiles/r02/multi4_k), but
+// the copy engines' all-to-all reaches only 0.57 of the link for groups of four (probe,
+// profiles/r02/multi4_r) against 0.86 for SM bulk traffic, so for P >= 3 the node-tier kernel
+// pushes too (4x2: ~194 vs ~255 us of link time by the probe rates; 8 GPUs, so not measured here).
+// DASO_BLOCKING_PUSH: 0 never, 1 default (as above), 2 always (also P = 2 node-tier kernels).
 int kernel_push_mode() {   // read per blocking batch, so a test can compare the transports
     const char* e = getenv("DASO_BLOCKING_PUSH");
     if (e && strcmp(e, "0") == 0) return 0;
@@ -325,9 +328,9 @@ int kernel_push_mode() {   // read per blocking batch, so a test can compare the
 }
 
 bool kernel_push_ok(daso_ctx* c, bool merge) {
-    const bool node_tier_kernel = c->cfg.mode == DASO_MODE_FUSED && c->G > 1;
+    const bool node_tier_kernel_p2 = c->cfg.mode == DASO_MODE_FUSED && c->G > 1 && c->P <= 2;
     return c->ce && c->exch_enabled && !merge && c->P > 1 && c->P - 1 <= daso::kMaxPush &&
-           kernel_push_mode() >= (node_tier_kernel ? 2 : 1);
+           kernel_push_mode() >= (node_tier_kernel_p2 ? 2 : 1);
 }
 
 daso_status kernel_push_prepare(daso_ctx* c, daso::KernelArgs& a, cudaStream_t s) {

@@ -198,7 +198,7 @@ def test_vcluster_full_size_2x4_sampled(wire):
                 np.testing.assert_array_equal(trace[j * G + l][k], trace[j * G][k])
 
 
-@pytest.mark.parametrize("P,G", [(2, 2), (2, 4)])
+@pytest.mark.parametrize("P,G", [(2, 2), (2, 4), (4, 2)])
 def test_vcluster_fused_trace_accounting(P, G, monkeypatch):
     """The library's per-launch byte accounting (daso_trace) for the fused node tier: a plain batch is
     one node-tier launch moving 2 (G-1) * 4 B per shard element over NVLink per direction (peer
@@ -213,8 +213,10 @@ def test_vcluster_fused_trace_accounting(P, G, monkeypatch):
     # a blocking batch's node-tier kernel also stores the packed bf16 row into the P-1 other group
     # members' slots (kernel push, DASO_BLOCKING_PUSH=2), 2 B per shard element each; with the default (1)
     # the copy engines push after the kernel (exchange bytes, not kernel bytes)
+    # (default mode 1: the node-tier kernel pushes for groups of P >= 3, the copy engines for P = 2)
     for B, S, ex, mode, launches, extra in [(4, 1, "nccl", "1", 1, 0.0), (1, 0, "nccl", "1", 2, 0.0),
-                                            (1, 0, "ce", "2", 2, (P - 1) * 2.0 * seg), (1, 0, "ce", "1", 2, 0.0)]:
+                                            (1, 0, "ce", "2", 2, (P - 1) * 2.0 * seg),
+                                            (1, 0, "ce", "1", 2, (P - 1) * 2.0 * seg if P >= 3 else 0.0)]:
         monkeypatch.setenv("DASO_BLOCKING_PUSH", mode)
         vc = daso.VCluster(P * G, G, B, S, d, total_epochs=1, steps_per_epoch=B * 64, mode="fused", exchange=ex)
         try:
@@ -234,7 +236,7 @@ def test_vcluster_fused_trace_accounting(P, G, monkeypatch):
             vc.destroy()
 
 
-@pytest.mark.parametrize("P,G", [(2, 2), (4, 1), (2, 4), (8, 1)])
+@pytest.mark.parametrize("P,G", [(2, 2), (4, 1), (2, 4), (8, 1), (4, 2)])
 def test_vcluster_blocking_kernel_push_equals_copy_engines(P, G, monkeypatch):
     """Blocking syncs with the CE transport: the pack kernel storing the packed row into every group
     member's slot (kernel push; DASO_BLOCKING_PUSH=2 also from the fused node-tier kernel at G > 1) and
