@@ -212,9 +212,9 @@ daso_status daso_global_merge(daso_ctx* c, void* stream);
  * kernel only packs (no parameter stores), the group exchange runs, then one kernel averages
  * the P rows of the shard and stores the result into every node peer's x, ending with the
  * node barrier.  With the copy-engine transport the local pack kernel of a blocking batch
- * (G = 1, sharded mode) stores the packed row straight into every group member's slot
- * (environment DASO_BLOCKING_PUSH: 0 never, 1 local pack kernels (default), 2 also the
- * fused node-tier kernel; DASO_AVG_PUBLISH=ldg|tma selects the tail's store path; all
+ * (G = 1, sharded mode; and the fused node-tier kernel for groups of P >= 3) stores the
+ * packed row straight into every group member's slot (environment DASO_BLOCKING_PUSH: 0 never,
+ * 1 default, 2 always; DASO_AVG_PUBLISH=ldg|tma selects the tail's store path; all
  * choices give bit-identical results).
  * `lr` is this batch's learning rate; `plateau` as in daso_sched_next.
  * Errors: DASO_ERR_PROTOCOL (not bound; schedule/flight-state mismatch), asynchronous
