@@ -417,6 +417,19 @@ def make_sleep(ms: float):
     return lambda: torch.cuda._sleep(cycles)
 
 
+def exposed_from_cycles(t_with, t_without):
+    """Exposed exchange time per cycle: the median of the paired differences of alternating cycles
+    (cycle 2i with the exchange, 2i+1 without): drift across the run cancels, only the drift between
+    the two adjacent cycles of a pair remains."""
+    return statistics.median([w - wo for w, wo in zip(t_with, t_without)])
+
+
+def hidden_fraction(exposed, n_exch_per_cycle, t_ag):
+    """1 - exposed / (exchanges per cycle x T_AG,alone); a cycle faster with the exchange
+    than without counts as fully hidden."""
+    return 1.0 - max(0.0, exposed) / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
+
+
 def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t_ag, cycles=None):
     """SURVEY §8(d) hidden fraction: hidden = 1 - (T_with - T_without) / T_AG,alone, per B-cycle.
     One cycle = B batches of [fwd/bwd stand-in (bf16 GEMMs) ; gradient refresh ; daso_step], timed by
@@ -428,8 +441,9 @@ def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t
     alternate block by block (a block is 1 cycle, or 2 when S = B so that the timed cycle's merge
     waits for an exchange of its own leg) to cancel clock and power drift; T_AG,alone is measured
     before the bench's first step (daso_exchange_alone).  The exposed time is the median of the
-    paired differences (cycle 2i with the exchange minus cycle 2i+1 without), which cancels drift
-    slower than two cycles; the difference of the two legs' medians is reported beside it."""
+    paired differences (cycle 2i with the exchange minus cycle 2i+1 without): drift across the run
+    cancels, only the drift within a pair remains; the difference of the two legs' medians is reported
+    beside it."""
     import torch
     block = 1 if a.S < a.B else 2
     cycles = cycles or a.cycles
@@ -460,8 +474,8 @@ def overlap_cycles(ctx, a, g, g_src, stream, world, compute, n_exch_per_cycle, t
     t_without = [e0.elapsed_time(e1) for e0, e1 in legs[False]]
     w_med = max_over_ranks(statistics.median(t_with), world)
     wo_med = max_over_ranks(statistics.median(t_without), world)
-    exposed = max_over_ranks(statistics.median([w - wo for w, wo in zip(t_with, t_without)]), world)
-    hidden = 1.0 - max(0.0, exposed) / (n_exch_per_cycle * t_ag) if t_ag > 0 else None
+    exposed = max_over_ranks(exposed_from_cycles(t_with, t_without), world)
+    hidden = hidden_fraction(exposed, n_exch_per_cycle, t_ag)
     spread = max_over_ranks(pct(t_without, 0.9) - pct(t_without, 0.1), world)
     return {"def": "1 - (T_cycle,with - T_cycle,without) / (exchanges per cycle x T_AG,alone); exposed = median of "
                    "the paired differences of alternating cycles, max over ranks; T_AG,alone before the first step",

@@ -42,3 +42,19 @@ def test_warmup_below_three_is_rejected():
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--warmup", "2"], capture_output=True,
                        text=True, timeout=300, cwd=ROOT)
     assert r.returncode != 0
+
+
+def test_hidden_fraction_estimator_cancels_drift():
+    """§8(d) hidden fraction from alternating cycles: a linear drift of the cycle time (clock / power)
+    20x the exchange over the run cancels in the paired differences except the one drift step inside
+    a pair; exposure is capped at [0, 1]."""
+    import bench
+    drift = [1.0 + 0.01 * i for i in range(40)]            # ms, 0.4 ms of drift over the run
+    t_with = [drift[2 * i] + 0.02 for i in range(20)]      # 20 us exposed per cycle
+    t_without = [drift[2 * i + 1] for i in range(20)]
+    exposed = bench.exposed_from_cycles(t_with, t_without)
+    assert abs(exposed - (0.02 - 0.01)) < 1e-12            # the pair's own 10 us drift step remains
+    assert abs(bench.hidden_fraction(exposed, 1, 0.05) - 0.8) < 1e-9
+    assert bench.hidden_fraction(-0.01, 1, 0.05) == 1.0    # faster with the exchange: fully hidden
+    assert bench.hidden_fraction(0.2, 4, 0.05) == 0.0
+    assert bench.hidden_fraction(0.01, 1, 0.0) is None
